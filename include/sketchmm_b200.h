@@ -1,0 +1,108 @@
+/*
+ * sketchmm_b200 — C ABI of the B200-native sketched-product hot path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA-runtime types in the
+ * signatures; `stream` is a cudaStream_t passed as void*).  Device pointers
+ * are marked [dev], host pointers [host].  Every entry point returns an int
+ * status: SMM_OK (0), SMM_ERR_INVALID (parameter/shape violation — the
+ * Python facade maps it to InvalidParameterError, mirroring the reference's
+ * validation which always happens before any kernel work), SMM_ERR_CUDA
+ * (launch/runtime failure -> RuntimeError) or SMM_ERR_WORKSPACE (caller
+ * workspace too small).  smm_last_error() returns a thread-local message.
+ * Calls never abort; they are re-entrant per stream (no hidden global state
+ * besides per-device attribute caches).  Caller-allocated buffers only.
+ *
+ * Each entry point replaces a reference interface (paths relative to
+ * /root/reference/pkg/src/sketchmm):
+ *   smm_hash_tables          hashing.py:134-144 (bucket_table / sign_table via
+ *                            bucket_many / sign_many, hashing.py:64-75)
+ *   smm_compress_workspace   sketch.py:402-417 (estimate_workspace_bytes; device part)
+ *   smm_compress_accumulate  sketch.py:238-260 `_run_kernel` -> the compress kernels
+ *                            sketch.py:152-177 / 192-218 (steps 1-3, accumulated
+ *                            over an inner-index range [k0, k1) — the k-shard unit)
+ *   smm_finalize             sketch.py:178-188 / 219-234 (single inverse transform,
+ *                            1/b scale) -> ProductSketch.polys
+ *   smm_extract              sketch.py:375-399 `decompress_all` (+ the heavy-hitter
+ *                            threshold of experiments.py:136-168 / BASELINE cfg5)
+ *   smm_transpose            sketch.py:305-307 (`at = ascontiguousarray(A.T)`)
+ *   smm_fwht_batched         transforms.py:37-49 / 100-127 (fwht_inplace, xor_convolve)
+ *   smm_fft_batched          transforms.py:52-74 / 130-175 (fft_forward, fft_inverse,
+ *                            cyclic_convolve)
+ */
+#ifndef SKETCHMM_B200_H
+#define SKETCHMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMM_OK 0
+#define SMM_ERR_INVALID 1
+#define SMM_ERR_CUDA 2
+#define SMM_ERR_WORKSPACE 3
+
+/* transform codes match the reference container codes (sketch.py:43) */
+#define SMM_VARIANT_FFT 0
+#define SMM_VARIANT_FWHT 1
+
+#define SMM_MAX_DEPTH 63
+
+int smm_abi_version(void);
+const char *smm_last_error(void);
+
+/* Bucket / sign tables for keys 0..n-1 of hash group `group` (0 = h1, 1 = h2,
+ * 2 = s1, 3 = s2).  words_host [host]: the 8*d packed hash words in draw order
+ * (hashing.py:146-152).  For groups 0/1 buckets_out [dev] (d x n uint32) is
+ * written; for groups 2/3 signs_out [dev] (d x n int8, values +-1). */
+int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int64_t n,
+                    uint32_t *buckets_out, int8_t *signs_out, void *stream);
+
+/* Device workspace (bytes) needed by smm_compress_accumulate for these shapes. */
+int smm_compress_workspace(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0,
+                           int64_t k1, int64_t *bytes);
+
+/* Steps 1-3 over inner indices [k0, k1):
+ *   at [dev]: row k = column k of A (k-major, leading dimension ld_at >= n1);
+ *   bm [dev]: row k = row k of B (leading dimension ld_bm >= n2).
+ * acc [dev] is OVERWRITTEN with the pre-inverse accumulator of this k-range:
+ *   FWHT: d x b float64;  FFT: d x (b/2+1) complex128 (interleaved re, im).
+ * Accumulators of disjoint k-ranges add (the multi-GPU allreduce unit). */
+int smm_compress_accumulate(int variant, const double *at, int64_t ld_at, const double *bm,
+                            int64_t ld_bm, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
+                            const uint64_t *words_host, int d, int log2b, void *acc,
+                            void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Step 4: polys [dev] (d x b float64) = inverse transform of acc, times 1/b. */
+int smm_finalize(int variant, const void *acc, double *polys, int d, int log2b, void *stream);
+
+/* Step 5 on output rows [r0, r1) (all n2 columns):
+ *   est [dev, nullable]: (r1-r0) x n2 float64, leading dimension ld_est;
+ *   heavy hitters: |est| > thr (strict != 0) or >= thr; *hh_count [dev] receives
+ *   the count; if hh_pairs [dev] is non-NULL, the (i, j) pairs (global row
+ *   index, column) are written in row-major order, at most hh_cap pairs.
+ *   workspace [dev] of smm_extract_workspace() bytes. */
+int smm_extract_workspace(int d, int64_t n1, int64_t n2, int64_t r0, int64_t r1, int64_t *bytes);
+int smm_extract(int variant, const double *polys, const uint64_t *words_host, int d, int log2b,
+                int64_t n1, int64_t n2, int64_t r0, int64_t r1, double *est, int64_t ld_est,
+                double thr, int strict, int64_t *hh_pairs, int64_t hh_cap, int64_t *hh_count,
+                void *workspace, int64_t workspace_bytes, void *stream);
+
+/* out[c, r] = in[r, c] for a rows x cols float64 matrix [dev]. */
+int smm_transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out,
+                  int64_t ld_out, void *stream);
+
+/* In-place unnormalized FWHT of `batch` contiguous vectors of length 2^log2n [dev],
+ * followed by a multiply by `scale`. */
+int smm_fwht_batched(double *x, int64_t batch, int log2n, double scale, void *stream);
+
+/* In-place complex FFT (interleaved complex128) of `batch` contiguous vectors of
+ * length 2^log2n [dev]; inverse != 0 uses conjugate twiddles; then * scale. */
+int smm_fft_batched(double *z, int64_t batch, int log2n, int inverse, double scale, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKETCHMM_B200_H */

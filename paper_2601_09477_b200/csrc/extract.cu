@@ -1,0 +1,234 @@
+// Step 5: estimate extraction (gather + sign + median over d) fused with the
+// heavy-hitter threshold.
+//
+// Reference: sketch.py:375-399 (`decompress_all`): idx = h1(i) ^ h2(j) (fwht)
+// or (h1(i) + h2(j)) mod b (fft); vals = polys[t, idx] * s1 * s2; median over
+// the d repetitions (odd d: the exact middle order statistic).  Threshold:
+// experiments.py:136-168 (|est| >= thr, inclusive) or BASELINE cfg5 (> thr).
+//
+// One CTA covers a tile of rows x 256 columns; each thread owns one column,
+// keeps its d (bucket, sign) pairs in registers and walks the rows, whose
+// hashes are evaluated once per CTA into shared memory.  The gathered sketch
+// values come from the L2-resident d x b polys.  Estimates are written with
+// coalesced stores (or skipped in threshold-only mode); the threshold writes a
+// bitmask + per-row counts so the pair list is emitted in row-major order by a
+// second pass (deterministic, no atomics on positions).
+#include "common.cuh"
+
+namespace smm {
+
+constexpr int XT = 256;
+constexpr int XROWS = 16;
+
+template <int D>
+__device__ __forceinline__ double median_sorted(double (&v)[D]) {
+#pragma unroll
+  for (int i = 1; i < D; ++i) {
+#pragma unroll
+    for (int j = i; j > 0; --j) {
+      const double a = v[j - 1], b = v[j];
+      const bool sw = b < a;  // compare-exchange keeps the exact values
+      v[j - 1] = sw ? b : a;
+      v[j] = sw ? a : b;
+    }
+  }
+  return v[(D - 1) / 2];
+}
+
+struct ExtractArgs {
+  SketchHashes h;
+  const double *polys;
+  int64_t n1, n2, r0, r1;
+  double *est;
+  int64_t ld_est;
+  double thr;
+  int strict, xor_combine;
+  uint32_t *mask;  // rows x ceil(n2/32)
+  int64_t mask_ld;
+  int64_t *rowcnt;  // rows
+};
+
+template <int D>
+__global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
+  const int d = D > 0 ? D : p.h.d;
+  constexpr int DM = D > 0 ? D : SMM_MAX_DEPTH;
+  __shared__ uint32_t s_h1[XROWS][DM];
+  __shared__ int8_t s_s1[XROWS][DM];
+  const int log2b = p.h.log2b;
+  const uint32_t bmask = (uint32_t)(((uint64_t)1 << log2b) - 1);
+  const int64_t b = (int64_t)1 << log2b;
+  const int64_t j = (int64_t)blockIdx.x * XT + threadIdx.x;
+  const int64_t rbase = p.r0 + (int64_t)blockIdx.y * XROWS;
+  const int nrows = (int)((p.r1 - rbase) < XROWS ? (p.r1 - rbase) : XROWS);
+  for (int q = threadIdx.x; q < nrows * d; q += XT) {
+    const int r = q / d, t = q % d;
+    s_h1[r][t] = eval_bucket(p.h.f[0][t], (uint64_t)(rbase + r), log2b);
+    s_s1[r][t] = eval_signbit(p.h.f[2][t], (uint64_t)(rbase + r)) ? -1 : 1;
+  }
+  __syncthreads();
+  const bool colok = j < p.n2;
+  uint32_t h2[DM];
+  double s2[DM];
+#pragma unroll
+  for (int t = 0; t < DM; ++t) {
+    if (t < d) {
+      h2[t] = colok ? eval_bucket(p.h.f[1][t], (uint64_t)j, log2b) : 0u;
+      s2[t] = (colok && eval_signbit(p.h.f[3][t], (uint64_t)j)) ? -1.0 : 1.0;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  for (int r = 0; r < nrows; ++r) {
+    const int64_t i = rbase + r;
+    double v[DM];
+#pragma unroll
+    for (int t = 0; t < DM; ++t) {
+      if (t < d) {
+        const uint32_t a = s_h1[r][t];
+        const uint32_t idx = p.xor_combine ? (a ^ h2[t]) : ((a + h2[t]) & bmask);
+        double x = colok ? __ldg(p.polys + t * b + idx) : 0.0;
+        x *= (double)s_s1[r][t];  // vals *= s1 ; vals *= s2 (sketch.py:396-397)
+        x *= s2[t];
+        v[t] = x;
+      }
+    }
+    double e;
+    if (D > 0) {
+      e = median_sorted<DM>(v);
+    } else {
+      for (int a = 1; a < d; ++a) {
+        double key = v[a];
+        int q = a - 1;
+        while (q >= 0 && v[q] > key) { v[q + 1] = v[q]; --q; }
+        v[q + 1] = key;
+      }
+      e = v[(d - 1) / 2];
+    }
+    if (colok && p.est) p.est[(i - p.r0) * p.ld_est + j] = e;
+    const double ae = fabs(e);
+    const bool hit = colok && (p.strict ? (ae > p.thr) : (ae >= p.thr));
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0 && (j >> 5) < p.mask_ld) {
+      p.mask[(i - p.r0) * p.mask_ld + (j >> 5)] = bal;
+      if (bal) atomicAdd((unsigned long long *)&p.rowcnt[i - p.r0], (unsigned long long)__popc(bal));
+    }
+  }
+}
+
+// exclusive scan of per-row counts (single block) -> offsets; total -> *count
+__global__ void row_scan_kernel(const int64_t *rowcnt, int64_t rows, int64_t *offs, int64_t *count) {
+  __shared__ int64_t s[1024];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < rows; base += 1024) {
+    const int64_t r = base + threadIdx.x;
+    int64_t v = r < rows ? rowcnt[r] : 0;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      int64_t add = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+      __syncthreads();
+      s[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (r < rows) offs[r] = carry + s[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+// one warp per row: emit (i, j) pairs in column order
+__global__ void hh_write_kernel(const uint32_t *mask, int64_t mask_ld, const int64_t *offs, int64_t rows, int64_t r0,
+                                int64_t n2, int64_t *pairs, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    int64_t pos = offs[r];
+    const uint32_t *mrow = mask + r * mask_ld;
+    for (int64_t w0 = 0; w0 < mask_ld; w0 += 32) {
+      const int64_t w = w0 + lane;
+      const uint32_t bits = w < mask_ld ? mrow[w] : 0u;
+      const int cnt = __popc(bits);
+      int incl = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int64_t p0 = pos + incl - cnt;
+      uint32_t bb = bits;
+      while (bb) {
+        const int bit = __ffs(bb) - 1;
+        bb &= bb - 1;
+        const int64_t jj = w * 32 + bit;
+        if (p0 < cap && jj < n2) {
+          pairs[2 * p0] = r0 + r;
+          pairs[2 * p0 + 1] = jj;
+        }
+        ++p0;
+      }
+      pos += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+int64_t extract_workspace(int64_t n2, int64_t r0, int64_t r1) {
+  const int64_t rows = r1 - r0;
+  const int64_t mask_ld = ceil_div(n2, 32);
+  return ((rows * mask_ld * 4 + 255) / 256) * 256 + 2 * ((rows * 8 + 255) / 256) * 256 + 256;
+}
+
+int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1, int64_t n2, int64_t r0, int64_t r1,
+            double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
+            int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s) {
+  const int64_t rows = r1 - r0;
+  if (ws_bytes < extract_workspace(n2, r0, r1)) {
+    set_error("extract workspace too small");
+    return SMM_ERR_WORKSPACE;
+  }
+  ExtractArgs p;
+  p.h = h;
+  p.polys = polys;
+  p.n1 = n1;
+  p.n2 = n2;
+  p.r0 = r0;
+  p.r1 = r1;
+  p.est = est;
+  p.ld_est = ld_est;
+  p.thr = thr;
+  p.strict = strict;
+  p.xor_combine = variant == SMM_VARIANT_FWHT ? 1 : 0;
+  p.mask_ld = ceil_div(n2, 32);
+  p.mask = (uint32_t *)ws;
+  char *q = ws + ((rows * p.mask_ld * 4 + 255) / 256) * 256;
+  p.rowcnt = (int64_t *)q;
+  int64_t *offs = (int64_t *)(q + ((rows * 8 + 255) / 256) * 256);
+  if (rows <= 0 || n2 <= 0) {
+    SMM_CUDA_TRY(cudaMemsetAsync(hh_count, 0, sizeof(int64_t), s), "extract memset");
+    return SMM_OK;
+  }
+  SMM_CUDA_TRY(cudaMemsetAsync(p.rowcnt, 0, rows * 8, s), "extract memset");
+  dim3 grid((unsigned)ceil_div(n2, XT), (unsigned)ceil_div(rows, XROWS));
+  switch (h.d) {
+    case 1: extract_kernel<1><<<grid, XT, 0, s>>>(p); break;
+    case 3: extract_kernel<3><<<grid, XT, 0, s>>>(p); break;
+    case 5: extract_kernel<5><<<grid, XT, 0, s>>>(p); break;
+    case 7: extract_kernel<7><<<grid, XT, 0, s>>>(p); break;
+    case 9: extract_kernel<9><<<grid, XT, 0, s>>>(p); break;
+    default: extract_kernel<0><<<grid, XT, 0, s>>>(p); break;
+  }
+  SMM_LAUNCH_CHECK("extract_kernel");
+  row_scan_kernel<<<1, 1024, 0, s>>>(p.rowcnt, rows, offs, hh_count);
+  SMM_LAUNCH_CHECK("row_scan_kernel");
+  if (hh_pairs && hh_cap > 0) {
+    int64_t blocks = ceil_div(rows * 32, 256);
+    if (blocks > 8192) blocks = 8192;
+    hh_write_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.mask, p.mask_ld, offs, rows, r0, n2, hh_pairs, hh_cap);
+    SMM_LAUNCH_CHECK("hh_write_kernel");
+  }
+  return SMM_OK;
+}
+
+}  // namespace smm

@@ -1,0 +1,240 @@
+// Hash tables and scatter plans (see plan.cuh).
+#include <cstdarg>
+#include <cstring>
+
+#include "plan.cuh"
+
+namespace smm {
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[512];
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char *last_error() { return g_err; }
+
+int cuda_status(cudaError_t e, const char *what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return SMM_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 1;
+  }
+  return cached[dev];
+}
+
+void load_hashes(SketchHashes &h, const uint64_t *words, int d, int log2b) {
+  memset(&h, 0, sizeof(h));
+  h.d = d;
+  h.log2b = log2b;
+  for (int g = 0; g < 4; ++g)
+    for (int t = 0; t < d; ++t) {
+      h.f[g][t].a = words[g * 2 * d + 2 * t];
+      h.f[g][t].c = words[g * 2 * d + 2 * t + 1];
+    }
+}
+
+// ------------------------------------------------------------------ hash tables
+__global__ void hash_table_kernel(SketchHashes h, int group, int64_t n, uint32_t *buckets, int8_t *signs) {
+  int t = blockIdx.y;
+  HashFn f = h.f[group][t];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    if (group < 2)
+      buckets[t * n + x] = eval_bucket(f, (uint64_t)x, h.log2b);
+    else
+      signs[t * n + x] = eval_signbit(f, (uint64_t)x) ? (int8_t)-1 : (int8_t)1;
+  }
+}
+
+int hash_tables(const SketchHashes &h, int group, int64_t n, uint32_t *buckets, int8_t *signs, cudaStream_t s) {
+  if (n <= 0) return SMM_OK;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > 4096) blocks = 4096;
+  hash_table_kernel<<<dim3((unsigned)blocks, h.d), 256, 0, s>>>(h, group, n, buckets, signs);
+  SMM_LAUNCH_CHECK("hash_table_kernel");
+  return SMM_OK;
+}
+
+// ------------------------------------------------------------------ plans
+__host__ __device__ static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
+
+int64_t plan_bytes_per(int64_t nin_max, int L) {
+  return pad256(nin_max * 4) + pad256((nin_max + 2) * 4) + pad256(((int64_t)1 << L) * 4) + 256 +
+         pad256((nin_max + 2) * 4) + pad256(nin_max * 4);
+}
+
+int64_t plan_total_bytes(int d, int nops, int64_t n1, int64_t n2, int L) {
+  int64_t nin_max = nops == 2 ? (n1 > n2 ? n1 : n2) : n1 + n2;
+  return (int64_t)d * nops * plan_bytes_per(nin_max, L);
+}
+
+struct PlanArgs {
+  SketchHashes h;
+  char *base;
+  int64_t per_bytes, nin_max, n1, n2;
+  int nops, L;
+  int smem_ints;
+};
+
+__device__ __forceinline__ uint32_t plan_bucket(const PlanArgs &p, int t, int op, int64_t q) {
+  // full bucket of input q of operand op under repetition t
+  if (p.nops == 2) return eval_bucket(p.h.f[op][t], (uint64_t)q, p.h.log2b);
+  return q < p.n1 ? eval_bucket(p.h.f[0][t], (uint64_t)q, p.h.log2b)
+                  : eval_bucket(p.h.f[1][t], (uint64_t)(q - p.n1), p.h.log2b);
+}
+
+constexpr int PLAN_THREADS = 512;
+
+__global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(PlanArgs p) {
+  extern __shared__ int sm[];  // p.smem_ints ints
+  __shared__ int s_red[32];
+  __shared__ int s_scan[PLAN_THREADS / 32 + 1];
+  const int t = blockIdx.x / p.nops, op = blockIdx.x % p.nops;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nin = p.nops == 2 ? (op == 0 ? p.n1 : p.n2) : p.n1 + p.n2;
+  const int64_t ell = (int64_t)1 << p.L;
+  const uint32_t cmask = (uint32_t)(ell - 1);
+  char *blk = p.base + (int64_t)(t * p.nops + op) * p.per_bytes;
+  uint32_t *list = (uint32_t *)blk;
+  blk += pad256(p.nin_max * 4);
+  int32_t *roff = (int32_t *)blk;
+  blk += pad256((p.nin_max + 2) * 4);
+  uint32_t *empty = (uint32_t *)blk;
+  blk += pad256(ell * 4);
+  int32_t *meta = (int32_t *)blk;
+  blk += 256;
+  int32_t *fill = (int32_t *)blk;
+  blk += pad256((p.nin_max + 2) * 4);
+  int32_t *rank = (int32_t *)blk;
+
+  int *run = sm;  // ell ints
+  for (int64_t c = tid; c < ell; c += PLAN_THREADS) run[c] = 0;
+  for (int64_t r = tid; r < nin + 2; r += PLAN_THREADS) roff[r] = 0;
+  __syncthreads();
+
+  // 1. ranks: one warp walks the inputs in order (deterministic by construction)
+  if (warp == 0) {
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = 0; base < nin; base += 32) {
+      int64_t q = base + lane;
+      bool valid = q < nin;
+      uint32_t c = valid ? (plan_bucket(p, t, op, q) & cmask) : (0x80000000u | (uint32_t)lane);
+      unsigned peers = __match_any_sync(0xffffffffu, c);
+      int b0 = valid ? run[c] : 0;
+      __syncwarp();
+      int r = b0 + __popc(peers & lt);
+      if (valid && lane == 31 - __clz(peers)) run[c] = b0 + __popc(peers);
+      __syncwarp();
+      if (valid) rank[q] = r;
+    }
+  }
+  __syncthreads();
+
+  // 2. nrounds = max bucket load; per-round sizes; empty buckets
+  int mx = 0;
+  for (int64_t c = tid; c < ell; c += PLAN_THREADS) mx = max(mx, run[c]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    int m = 0;
+    for (int w = 0; w < PLAN_THREADS / 32; ++w) m = max(m, s_red[w]);
+    meta[0] = m;
+  }
+  for (int64_t c = tid; c < ell; c += PLAN_THREADS)
+    for (int r = 0; r < run[c]; ++r) atomicAdd(&roff[r + 1], 1);
+  // ordered compaction of empty buckets
+  int running = 0;
+  for (int64_t c0 = 0; c0 < ell; c0 += PLAN_THREADS) {
+    int64_t c = c0 + tid;
+    bool e = c < ell && run[c] == 0;
+    unsigned bal = __ballot_sync(0xffffffffu, e);
+    if (lane == 0) s_scan[warp] = __popc(bal);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < PLAN_THREADS / 32; ++w) {
+        int v = s_scan[w];
+        s_scan[w] = acc;
+        acc += v;
+      }
+      s_scan[PLAN_THREADS / 32] = acc;
+    }
+    __syncthreads();
+    if (e) empty[running + s_scan[warp] + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)c;
+    running += s_scan[PLAN_THREADS / 32];
+    __syncthreads();
+  }
+  if (tid == 0) meta[1] = running;
+  __syncthreads();
+
+  // 3. round offsets (exclusive scan of per-round sizes)
+  const int nrounds = meta[0];
+  if (tid == 0) {
+    int acc = 0;
+    for (int r = 0; r <= nrounds; ++r) {
+      acc += roff[r];
+      roff[r] = acc;  // roff[0] = 0, roff[r] = start of round r
+    }
+  }
+  __syncthreads();
+
+  // 4. placement: one warp, inputs in order; per-round fill pointers in smem when they fit
+  const bool fill_in_smem = nrounds + 1 <= p.smem_ints;
+  int *fs = sm;
+  for (int r = tid; r <= nrounds; r += PLAN_THREADS) {
+    if (fill_in_smem) fs[r] = roff[r];
+    else fill[r] = roff[r];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned lt = (1u << lane) - 1u;
+    int *fp = fill_in_smem ? fs : (int *)fill;
+    for (int64_t base = 0; base < nin; base += 32) {
+      int64_t q = base + lane;
+      bool valid = q < nin;
+      int r = valid ? rank[q] : (int)(0x80000000u | (uint32_t)lane);
+      unsigned peers = __match_any_sync(0xffffffffu, r);
+      int b0 = valid ? fp[r] : 0;
+      __syncwarp();
+      if (valid && lane == 31 - __clz(peers)) fp[r] = b0 + __popc(peers);
+      __syncwarp();
+      if (valid) list[b0 + __popc(peers & lt)] = (uint32_t)q;
+    }
+  }
+}
+
+int build_plans(const SketchHashes &h, int nops, int64_t n1, int64_t n2, int L, char *ws, cudaStream_t s) {
+  PlanArgs p;
+  p.h = h;
+  p.base = ws;
+  p.nin_max = nops == 2 ? (n1 > n2 ? n1 : n2) : n1 + n2;
+  p.per_bytes = plan_bytes_per(p.nin_max, L);
+  p.n1 = n1;
+  p.n2 = n2;
+  p.nops = nops;
+  p.L = L;
+  int64_t ell = (int64_t)1 << L;
+  int ints = (int)(ell > 4096 ? ell : 4096);
+  p.smem_ints = ints;
+  size_t smem = (size_t)ints * 4;
+  SMM_CUDA_TRY(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "plan_kernel smem");
+  plan_kernel<<<h.d * nops, PLAN_THREADS, smem, s>>>(p);
+  SMM_LAUNCH_CHECK("plan_kernel");
+  return SMM_OK;
+}
+
+}  // namespace smm
