@@ -1,0 +1,377 @@
+"""Benchmark of the sketched-product hot path on B200 (BASELINE.json metric).
+
+Workload: BASELINE cfg3 — n = 16384 float64, FWHT variant, b = 2^16, d = 5,
++-1 operands with 256 planted heavy entries (paper_2601_09477_b200/workloads.py),
+heavy-hitter threshold |est| > n/2.  One *step* is one complete sketched
+product through the public API on device-resident operands:
+  compress (A^T transpose, hash plans, fused fold-scatter + FWHT + product +
+  accumulate, CTA-partial reduction, inverse FWHT and 1/b) followed by
+  extraction of all n^2 median estimates (materialised in HBM) fused with the
+  heavy-hitter threshold and the row-major pair list.
+Metric: milliseconds per sketched product (lower is better).  With N ranks
+(torchrun) the inner dimension is sharded (k-slab per rank), the d x b
+accumulators are summed with one NCCL allreduce, and output rows are sharded:
+same total work, strong scaling; the reported time is the max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+bit-exact C/OpenMP oracle port, oracle/, all host cores) on a bounded k-slice /
+row-slice sample of the same workload, extrapolated to the full product.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sketched_product_ms_n16384_fp64"
+UNIT = "ms"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# measured on this pool's B200 by tools/microbench.cu (profiles/r01_microbench.txt):
+# DADD 18.52 Tops/s = 63.7 FP64-pipe ops/clk/SM at 1965 MHz (burst, kernel timed alone)
+FP64_PIPE_PEAK_TOPS = 18.52
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def _oracle_sample(w, k_slice: int, row_slice: int, threads: int):
+    """Time the CPU oracle (reference algorithm, bit-exact port) on a bounded sample of w."""
+    from oracle import sketch_oracle as O
+
+    words = O.draw_words(w.sketch_seed, w.d, w.b)
+    at = np.ascontiguousarray(w.a[:, :k_slice].T)  # rows k of A^T for the k-slice (as the reference copies A.T)
+    bm = np.ascontiguousarray(w.bmat[:k_slice])
+    t0 = time.perf_counter()
+    acc = O.accumulate_fwht(at, bm, b=w.b, d=w.d, words=words, k0=0, k1=k_slice, threads=threads)
+    tk = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    polys = O.fwht_inverse_scaled(acc)
+    tf = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, r0=0, r1=row_slice,
+                 want_est=True, thr=w.threshold, strict=True, threads=threads)
+    tr = time.perf_counter() - t0
+    full_ms = (tk * w.n / k_slice + tf + tr * w.n / row_slice) * 1e3
+    return full_ms, {"k_slice": k_slice, "row_slice": row_slice, "t_k_s": tk, "t_rows_s": tr, "t_inv_s": tf}
+
+
+def _cpu_instance(cfg: str):
+    from paper_2601_09477_b200 import workloads as W
+
+    return W.make(cfg)
+
+
+def _calibrate(w, threads: int, budget_s: float):
+    _, info = _oracle_sample(w, 16, 64, threads)
+    per_k = info["t_k_s"] / 16
+    per_row = info["t_rows_s"] / 64
+    k_slice = int(min(w.n, max(16, (0.7 * budget_s) / max(per_k, 1e-9))))
+    row_slice = int(min(w.n, max(64, (0.3 * budget_s) / max(per_row, 1e-9))))
+    return k_slice, row_slice
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import sketch_oracle as O
+
+    O.build()
+    threads = O.cpu_count()
+    w = _cpu_instance(args.config)
+    k_slice, row_slice = _calibrate(w, threads, args.ref_step_budget)
+    times = []
+    info = None
+    for step in range(args.warmup + args.steps):
+        ms, info = _oracle_sample(w, k_slice, row_slice, threads)
+        if step >= args.warmup:
+            times.append(ms)
+    value = float(np.median(times))
+    sample = (f"oracle C/OpenMP port (bit-exact vs reference Numba kernels): compress k-slice of {k_slice}/{w.n} "
+              f"inner indices + inverse + decompress/threshold of {row_slice}/{w.n} rows, extrapolated linearly "
+              f"to the full n={w.n} product per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg3 construction)",
+            "config": _config(args, w.n, w.b, w.d),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sample_detail": info}
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, n, b, d):
+    return {"workload": f"BASELINE {args.config}: n={n} fp64 FWHT b={b} d={d}, +-1 operands with 256 planted "
+                        f"entries, heavy-hitter threshold |est|>n/2; compress + inverse + full n^2 extraction + threshold",
+            "n": n, "b": b, "d": d, "transform": "fwht", "parallelism": f"k-shard x{args.gpus} + 1 allreduce",
+            "l2": "operands (2 x 2 GiB) exceed the 126 MB L2; no flush needed between steps"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_09477_b200 as P
+    from paper_2601_09477_b200 import _device, _lib, workloads as W
+    from paper_2601_09477_b200.distributed import compress_sharded, row_bounds, shard_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    w = W.make(args.config, xp=torch, device=dev)
+    n, b, d = w.n, w.b, w.d
+    params = P.SketchParams(n=n, b=b, d=d, transform=w.transform, seed=w.sketch_seed)
+    k0, k1 = shard_bounds(n, world, rank)
+    r0, r1 = row_bounds(n, world, rank)
+    # this rank's device-resident inputs: the k-slab of A (columns) and of B (rows)
+    a_slab = w.a[:, k0:k1].contiguous()
+    b_slab = w.bmat[k0:k1].contiguous()
+    del w.a, w.bmat
+    torch.cuda.empty_cache()
+    est_buf = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+
+    def step():
+        if world == 1:
+            sk = P.compress(a_slab, b_slab, params)
+        else:
+            at = _device.transpose(a_slab)
+            sk = compress_sharded(at, b_slab, params, n_rows=n, n_cols=n)
+        est, pairs = P.extract_all(sk, w.threshold, strict=True, r0=r0, r1=r1, est_out=est_buf)
+        return sk, est, pairs
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = lib.smm_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            sk, est, pairs = step()
+        ev1.record()
+        barrier()
+    launches = lib.smm_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    hh_local = int(pairs.shape[0])
+
+    # ---- kernel-level timing of the dominant kernel (compress accumulate) for the roofline
+    words = sk.words
+    at_full = _device.transpose(a_slab)
+    kl = k1 - k0
+    for _ in range(2):
+        acc = _device.compress_accumulate(at_full, b_slab, words, d, params.log2b, "fwht", 0, kl)
+    torch.cuda.synchronize()
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        acc = _device.compress_accumulate(at_full, b_slab, words, d, params.log2b, "fwht", 0, kl)
+    e1.record()
+    torch.cuda.synchronize()
+    t_comp = e0.elapsed_time(e1) / reps
+    e0.record()
+    for _ in range(reps):
+        P.extract_all(sk, w.threshold, strict=True, r0=r0, r1=r1, est_out=est_buf)
+    e1.record()
+    torch.cuda.synchronize()
+    t_extract = e0.elapsed_time(e1) / reps
+    logb = params.log2b
+    # algorithmic FP64-pipe ops of one accumulate launch: 2 forward transforms per (k, t),
+    # one product-accumulate FMA per bucket, one signed scatter-add per input element
+    ops = 2 * d * kl * b * logb + d * kl * b + 2 * d * kl * n
+    achieved = ops / (t_comp * 1e-3) / 1e12
+    hbm_bytes = 16 * n * kl + 8 * d * b
+    roofline = {"bound": "fp64", "kernel": "fwht_fold_kernel (smm_compress_accumulate)", "achieved": achieved,
+                "peak": FP64_PIPE_PEAK_TOPS, "unit": "Tops/s", "frac": achieved / FP64_PIPE_PEAK_TOPS,
+                "traffic": None, "algorithmic_ops": ops, "kernel_ms": t_comp,
+                "peak_source": "measured DADD pipe rate, tools/microbench.cu (profiles/r01_microbench.txt); "
+                               "MEASURED_PEAKS.json holds no FP64 figure",
+                "hbm": {"algorithmic_bytes": hbm_bytes, "achieved_gbs": hbm_bytes / (t_comp * 1e-3) / 1e9,
+                        "peak_gbs": _peaks().get("hbm_gbs"),
+                        "frac": hbm_bytes / (t_comp * 1e-3) / 1e9 / _peaks().get("hbm_gbs", 6650.0)},
+                "extract": {"ms": t_extract, "algorithmic_bytes": 8 * (r1 - r0) * n,
+                            "achieved_gbs": 8 * (r1 - r0) * n / (t_extract * 1e-3) / 1e9}}
+    traffic_file = ROOT / "profiles" / "r01_compress_dram_bytes.json"
+    if traffic_file.exists():
+        try:
+            roofline["traffic"] = json.loads(traffic_file.read_text()).get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            pass
+
+    # ---- e2e through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        a_host = a_slab.cpu().pin_memory()
+        b_host = b_slab.cpu().pin_memory()
+        est_host = torch.empty((r1 - r0, n), dtype=torch.float64).pin_memory()
+        del at_full, acc
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            if world == 1:
+                sk2 = P.compress(a_host, b_host, params)
+            else:
+                at = _device.transpose(a_host.to(dev, non_blocking=True))
+                sk2 = compress_sharded(at, b_host.to(dev, non_blocking=True), params, n_rows=n, n_cols=n)
+            est2, pairs2 = P.extract_all(sk2, w.threshold, strict=True, r0=r0, r1=r1, est_out=est_buf)
+            est_host.copy_(est2, non_blocking=True)
+            return pairs2.to("cpu")
+
+        e2e_step()
+        barrier()
+        e0.record()
+        e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(e2e_steps):
+            hp = e2e_step()
+        e1.record()
+        barrier()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(e2e_ms.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(a_host.numel() * 8 + b_host.numel() * 8),
+               "d2h_bytes_per_step": int(est_host.numel() * 8 + hp.numel() * 8),
+               "path": "paper_2601_09477_b200.compress(pinned host tensors) + extract_all + D2H of the estimate rows "
+                       "and heavy-hitter pairs"}
+
+    # ---- CPU baseline (rank 0, N=1): bounded oracle sample on the host cores
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import sketch_oracle as O
+
+        O.build()
+        threads = O.cpu_count()
+        wc = _cpu_instance(args.config)
+        k_slice, row_slice = _calibrate(wc, threads, args.cpu_budget)
+        full_ms, info = _oracle_sample(wc, k_slice, row_slice, threads)
+        cpu_baseline = {"value": full_ms, "unit": UNIT, "cores": threads, "kind": "port",
+                        "sample": f"oracle C/OpenMP port on {threads} host threads: compress k-slice {k_slice}/{n}, "
+                                  f"decompress+threshold rows {row_slice}/{n}, extrapolated to the full product",
+                        "detail": info}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg3 construction, seeded)",
+                "config": _config(args, n, b, d), "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary(),
+                "breakdown_ms": {"compress_accumulate": t_comp, "extract_all": t_extract},
+                "heavy_hitters_rank0": hh_local}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
+    ap.add_argument("--ref-step-budget", type=float, default=4.0, help="seconds per --impl reference step")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,18 @@ int smm_extract(int variant, const double *polys, const uint64_t *words_host, in
                 double thr, int strict, int64_t *hh_pairs, int64_t hh_cap, int64_t *hh_count,
                 void *workspace, int64_t workspace_bytes, void *stream);
 
+/* Heavy-hitter pair list of the LAST smm_extract call made with this workspace:
+ * the (i, j) pairs whose bit is set, in row-major order, at most hh_cap pairs
+ * (hh_pairs [dev], int64 pairs).  Needs no recomputation of the medians, so a
+ * caller can size hh_pairs from *hh_count of the extract call.  Replaces the
+ * thresholding loop of experiments.py:136-168. */
+int smm_hh_pairs(const void *workspace, int64_t n2, int64_t r0, int64_t r1, int64_t *hh_pairs, int64_t hh_cap,
+                 void *stream);
+
+/* Number of kernels this library has launched in the process (monotone counter;
+ * bench/evidence only). */
+int64_t smm_kernel_launches(void);
+
 /* out[c, r] = in[r, c] for a rows x cols float64 matrix [dev]. */
 int smm_transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out,
                   int64_t ld_out, void *stream);

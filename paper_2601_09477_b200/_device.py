@@ -134,10 +134,8 @@ def extract(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant:
         cnt = int(count.item())
         pairs = torch.empty((cnt, 2), dtype=torch.int64, device=dev)
         if cnt:
-            count2 = torch.zeros(1, dtype=torch.int64, device=dev)
-            _lib.check(lib.smm_extract(v, ptr(polys), wp, d, log2b, n1, n2, r0, r1, None, n2, float(thr),
-                                       1 if strict else 0, ptr(pairs), cnt, ptr(count2), ptr(ws), ws.numel(),
-                                       stream_ptr(dev)))
+            # the bitmask of this extract call is still in `ws`: emit pairs without recomputing medians
+            _lib.check(lib.smm_hh_pairs(ptr(ws), n2, r0, r1, ptr(pairs), cnt, stream_ptr(dev)))
     return est, count, pairs
 
 

@@ -31,6 +31,8 @@ EXPORTS = (
     "smm_finalize",
     "smm_extract_workspace",
     "smm_extract",
+    "smm_hh_pairs",
+    "smm_kernel_launches",
     "smm_transpose",
     "smm_fwht_batched",
     "smm_fft_batched",
@@ -71,6 +73,8 @@ def load():
             "smm_finalize": ([I, P, P, I, I, P], I),
             "smm_extract_workspace": ([I, I64, I64, I64, I64, P], I),
             "smm_extract": ([I, P, P, I, I, I64, I64, I64, I64, P, I64, D, I, P, I64, P, P, I64, P], I),
+            "smm_hh_pairs": ([P, I64, I64, I64, P, I64, P], I),
+            "smm_kernel_launches": ([], I64),
             "smm_transpose": ([P, I64, I64, I64, P, I64, P], I),
             "smm_fwht_batched": ([P, I64, I, D, P], I),
             "smm_fft_batched": ([P, I64, I, I, D, P], I),

@@ -19,6 +19,8 @@ int64_t extract_workspace(int64_t n2, int64_t r0, int64_t r1);
 int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1, int64_t n2, int64_t r0, int64_t r1,
             double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
             int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s);
+int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs, int64_t cap, cudaStream_t s);
+int64_t launches();
 int transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out, int64_t ld_out,
               cudaStream_t s);
 int fwht_batched(double *x, int64_t batch, int log2n, double scale, cudaStream_t s);
@@ -128,6 +130,16 @@ int smm_extract(int variant, const double *polys, const uint64_t *words_host, in
   return extract(variant, h, polys, n1, n2, r0, r1, est, ld_est, thr, strict, hh_pairs, hh_cap, hh_count,
                  (char *)workspace, workspace_bytes, (cudaStream_t)stream);
 }
+
+int smm_hh_pairs(const void *workspace, int64_t n2, int64_t r0, int64_t r1, int64_t *hh_pairs, int64_t hh_cap,
+                 void *stream) {
+  SMM_REQUIRE(workspace != nullptr, "workspace is NULL");
+  SMM_REQUIRE(r0 >= 0 && r1 >= r0 && n2 >= 0 && hh_cap >= 0, "bad ranges");
+  SMM_REQUIRE(hh_cap == 0 || hh_pairs != nullptr, "hh_pairs is NULL");
+  return smm::hh_pairs(workspace, n2, r0, r1, hh_pairs, hh_cap, (cudaStream_t)stream);
+}
+
+int64_t smm_kernel_launches(void) { return launches(); }
 
 int smm_transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out, int64_t ld_out,
                   void *stream) {

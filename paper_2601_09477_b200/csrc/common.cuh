@@ -16,7 +16,12 @@ int cuda_status(cudaError_t e, const char *what);
     cudaError_t _e = (expr);                              \
     if (_e != cudaSuccess) return ::smm::cuda_status(_e, what); \
   } while (0)
-#define SMM_LAUNCH_CHECK(what) SMM_CUDA_TRY(cudaGetLastError(), what)
+void count_launch();
+#define SMM_LAUNCH_CHECK(what)  \
+  do {                          \
+    ::smm::count_launch();      \
+    SMM_CUDA_TRY(cudaGetLastError(), what); \
+  } while (0)
 
 int num_sms();
 

@@ -174,6 +174,8 @@ __global__ void hh_write_kernel(const uint32_t *mask, int64_t mask_ld, const int
   }
 }
 
+int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs, int64_t cap, cudaStream_t s);
+
 int64_t extract_workspace(int64_t n2, int64_t r0, int64_t r1) {
   const int64_t rows = r1 - r0;
   const int64_t mask_ld = ceil_div(n2, 32);
@@ -222,12 +224,21 @@ int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1,
   SMM_LAUNCH_CHECK("extract_kernel");
   row_scan_kernel<<<1, 1024, 0, s>>>(p.rowcnt, rows, offs, hh_count);
   SMM_LAUNCH_CHECK("row_scan_kernel");
-  if (hh_pairs && hh_cap > 0) {
-    int64_t blocks = ceil_div(rows * 32, 256);
-    if (blocks > 8192) blocks = 8192;
-    hh_write_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.mask, p.mask_ld, offs, rows, r0, n2, hh_pairs, hh_cap);
-    SMM_LAUNCH_CHECK("hh_write_kernel");
-  }
+  if (hh_pairs && hh_cap > 0) return smm::hh_pairs(ws, n2, r0, r1, hh_pairs, hh_cap, s);
+  return SMM_OK;
+}
+
+int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs, int64_t cap, cudaStream_t s) {
+  const int64_t rows = r1 - r0;
+  if (rows <= 0 || n2 <= 0 || cap <= 0) return SMM_OK;
+  const int64_t mask_ld = ceil_div(n2, 32);
+  const uint32_t *mask = (const uint32_t *)ws;
+  const char *q = (const char *)ws + ((rows * mask_ld * 4 + 255) / 256) * 256;
+  const int64_t *offs = (const int64_t *)(q + ((rows * 8 + 255) / 256) * 256);
+  int64_t blocks = ceil_div(rows * 32, 256);
+  if (blocks > 8192) blocks = 8192;
+  hh_write_kernel<<<(unsigned)blocks, 256, 0, s>>>(mask, mask_ld, offs, rows, r0, n2, pairs, cap);
+  SMM_LAUNCH_CHECK("hh_write_kernel");
   return SMM_OK;
 }
 

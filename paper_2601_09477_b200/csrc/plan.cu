@@ -1,5 +1,6 @@
 // Hash tables and scatter plans (see plan.cuh).
 #include <cstdarg>
+#include <atomic>
 #include <cstring>
 
 #include "plan.cuh"
@@ -21,6 +22,10 @@ int cuda_status(cudaError_t e, const char *what) {
   set_error("%s: %s", what, cudaGetErrorString(e));
   return SMM_ERR_CUDA;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launches() { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
   static int cached[64] = {0};

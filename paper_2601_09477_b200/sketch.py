@@ -223,12 +223,13 @@ def compress(a, b, params: SketchParams, threads: int | None = None, device=None
     """Sketch the product of square n x n operands (sketch.py:289-302)."""
     from . import _device
 
-    dev = _device.require_cuda(device)
     sa = _check_2d(a, "left operand")
     sb = _check_2d(b, "right operand")
     n = params.n
     if sa != (n, n) or sb != (n, n):
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
+    effective_threads(threads)
+    dev = _device.require_cuda(device)
     av = _as_matrix(a, "left operand", dev)
     bv = _as_matrix(b, "right operand", dev)
     at = _device.transpose(av)  # the reference's ascontiguousarray(A.T) (sketch.py:305-307), on device
@@ -240,12 +241,13 @@ def compress_pretransposed(at, b, params: SketchParams, threads: int | None = No
     """Like ``compress`` with A given transposed (sketch.py:310-321)."""
     from . import _device
 
-    dev = _device.require_cuda(device)
     sa = _check_2d(at, "left operand (transposed)")
     sb = _check_2d(b, "right operand")
     n = params.n
     if sa != (n, n) or sb != (n, n):
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
+    effective_threads(threads)
+    dev = _device.require_cuda(device)
     return _run(_as_matrix(at, "left operand (transposed)", dev), _as_matrix(b, "right operand", dev), params, threads)
 
 
@@ -253,11 +255,12 @@ def compress_rect(a, b, params: SketchParams, threads: int | None = None, device
     """Sketch a rectangular product A (n1 x m) @ B (m x n2), m = params.n (sketch.py:324-340)."""
     from . import _device
 
-    dev = _device.require_cuda(device)
     sa = _check_2d(a, "left operand")
     sb = _check_2d(b, "right operand")
     if sa[1] != params.n or sb[0] != params.n:
         raise InvalidParameterError(f"inner dimension must equal params.n={params.n}, got {sa} x {sb}")
+    effective_threads(threads)
+    dev = _device.require_cuda(device)
     av = _as_matrix(a, "left operand", dev)
     at = _device.transpose(av)
     del av
@@ -345,6 +348,23 @@ def heavy_hitters(sketch: ProductSketch, threshold: float = 0.5, strict: bool = 
     return (pairs, est) if with_estimates else pairs
 
 
+def extract_all(sketch: ProductSketch, threshold: float = 0.5, strict: bool = True, *, r0: int = 0,
+                r1: int | None = None, device=None, est_out=None):
+    """Step 5 in one pass: the estimate rows [r0, r1) and their heavy-hitter pairs
+    (CUDA tensors).  This is ``decompress_all`` fused with the threshold."""
+    from . import _device
+
+    r1 = sketch.n_rows if r1 is None else r1
+    if not (0 <= r0 <= r1 <= sketch.n_rows):
+        raise InvalidParameterError(f"row range [{r0}, {r1}) outside {sketch.n_rows} rows")
+    p = sketch.params
+    polys = sketch.polys_device(device)
+    est, _, pairs = _device.extract(polys, sketch.words, p.d, p.log2b, p.transform, sketch.n_rows, sketch.n_cols,
+                                    r0, r1, want_est=True, thr=threshold, strict=strict, want_pairs=True,
+                                    est_out=est_out)
+    return est, pairs
+
+
 def estimate_workspace_bytes(n: int, b: int, d: int, transform: str, threads: int) -> int:
     """Host-memory estimate of the reference path (sketch.py:402-417), kept for API parity."""
     f8, c16 = 8, 16
@@ -419,7 +439,7 @@ def load_sketch(path) -> ProductSketch:
 
 __all__ = [
     "HashPair", "ProductSketch", "SketchParams", "TRANSFORMS", "combine_index", "compress", "compress_pretransposed",
-    "compress_rect", "decompress_all", "decompress_entry", "decompress_rows", "derive_params",
+    "compress_rect", "decompress_all", "decompress_entry", "decompress_rows", "derive_params", "extract_all",
     "device_workspace_bytes", "effective_threads", "estimate_workspace_bytes", "heavy_hitters", "load_sketch",
     "save_sketch", "sketch_estimates", "sketch_from_bytes", "sketch_to_bytes", "check_buckets",
 ]

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference goldens
+and the CPU oracle.  Run on a B200 with ``pytest -m gpu``.
+
+Tolerances (BASELINE north star): hash buckets/signs bit-exact; sketch values
+and estimates within 1e-10 * ||C||_F; heavy-hitter sets identical.  cfg3 is
+integer-valued, so its sketch must be bit-identical to the reference.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_09477_b200 as P
+from conftest import cfg_golden
+from oracle import sketch_oracle as O
+from paper_2601_09477_b200 import _device
+from paper_2601_09477_b200 import workloads as W
+from paper_2601_09477_b200.hashing import SketchHashes
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10  # relative to ||C||_F
+
+
+def _sha(x):
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+def _cnorm(a, bm):
+    return float(np.linalg.norm(np.asarray(a) @ np.asarray(bm)))
+
+
+def test_native_library_loaded_and_kernels_run():
+    from paper_2601_09477_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.smm_abi_version() == 1
+    sk = P.compress(np.eye(4), np.eye(4), P.SketchParams(n=4, b=16, d=1, seed=5))
+    assert isinstance(sk.polys_device(), torch.Tensor) and sk.polys_device().is_cuda
+
+
+def test_small_cases_match_reference(small_cases):
+    for c in small_cases:
+        p = P.SketchParams(n=c["m"], b=c["b"], d=c["d"], transform=c["transform"], seed=c["seed"])
+        rect = c["n1"] != c["m"] or c["n2"] != c["m"]
+        sk = P.compress_rect(c["a"], c["bm"], p) if rect else P.compress(c["a"], c["bm"], p, threads=c["threads"])
+        assert np.array_equal(sk.words, c["words"])
+        scale = max(1.0, _cnorm(c["a"], c["bm"]))
+        assert np.max(np.abs(sk.polys - c["polys"])) <= TOL * scale, c["name"]
+        est = P.decompress_all(sk)
+        assert est.shape == c["est"].shape
+        assert np.max(np.abs(est - c["est"])) <= TOL * scale, c["name"]
+
+
+def test_hash_tables_bit_exact(hash_golden):
+    for tab in hash_golden["tables"]:
+        a, c, shift = int(tab["a"]), int(tab["c"]), tab["shift"]
+        b = 1 << (64 - shift)
+        words = np.array([a, c, a, c, a, c, a, c], dtype=np.uint64)
+        h = SketchHashes.from_words(words, 1, b)
+        buckets = _device.hash_table(h, 0, 2000).cpu().numpy().astype(np.int64)[0]
+        signs = _device.hash_table(h, 2, 2000).cpu().numpy().astype(int)[0]
+        assert buckets.tolist() == tab["buckets"]
+        assert signs.tolist() == tab["signs"]
+
+
+def test_hash_tables_match_oracle_on_config_sizes():
+    for seed, d, b, n in ((203, 5, 1 << 16, 16384), (204, 7, 1 << 18, 32768), (7, 3, 1 << 32, 5000)):
+        words = O.draw_words(seed, d, b)
+        h = SketchHashes.from_words(words, d, b)
+        h1, s1, h2, s2 = O.tables(words, d, b, n, n)
+        assert np.array_equal(_device.hash_table(h, 0, n).cpu().numpy().astype(np.int64), h1)
+        assert np.array_equal(_device.hash_table(h, 1, n).cpu().numpy().astype(np.int64), h2)
+        assert np.array_equal(_device.hash_table(h, 2, n).cpu().numpy().astype(np.float64), s1)
+        assert np.array_equal(_device.hash_table(h, 3, n).cpu().numpy().astype(np.float64), s2)
+
+
+CONFIGS = ["cfg1", "cfg2", "cfg3", "cfg5_b12_d3_nnz512_fwht", "cfg5_b12_d9_nnz512_fft", "cfg5_b14_d5_nnz512_fwht",
+           "cfg5_b14_d3_nnz512_fft", "cfg5_b16_d9_nnz512_fwht", "cfg5_b16_d5_nnz512_fft"]
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_config_matches_reference(name):
+    g = cfg_golden(name)
+    if g is None:
+        pytest.skip(f"no golden for {name}")
+    w = W.make(name, xp=torch, device="cuda")
+    p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+    sk = P.compress(w.a, w.bmat, p)
+    assert np.array_equal(sk.words, g["words"])
+    cn = float(g["cnorm"][0])
+    if not np.isfinite(cn):
+        cn = float(torch.linalg.norm(w.a @ w.bmat))
+    polys = sk.polys
+    if name == "cfg3":
+        assert _sha(polys) == bytes(g["polys_sha256"]).decode()  # integer-exact: bit-identical
+    elif "polys" in g:
+        assert np.max(np.abs(polys - g["polys"])) <= TOL * cn
+    samp = np.take_along_axis(polys, g["polys_sample_idx"], axis=1)
+    assert np.max(np.abs(samp - g["polys_sample"])) <= TOL * cn
+    assert np.allclose(polys.sum(axis=1), g["polys_rowsum"], rtol=0, atol=TOL * cn * w.b)
+    est = P.decompress_rows(sk)
+    ij = torch.as_tensor(g["est_sample_ij"], device="cuda")
+    e = est[ij[:, 0], ij[:, 1]].cpu().numpy()
+    assert np.max(np.abs(e - g["est_sample"])) <= TOL * cn
+    big = torch.as_tensor(w.big, device="cuda")
+    if big.numel():
+        eb = est[big[:, 0], big[:, 1]].cpu().numpy()
+        assert np.max(np.abs(eb - g["est_big"])) <= TOL * cn
+    hh = P.heavy_hitters(sk, w.threshold, strict=True)
+    assert hh.shape[0] == int(g["hh_count"][0])
+    assert _sha(hh.astype(np.int64)) == bytes(g["hh_sha256"]).decode()
+
+
+def test_cfg3_k_slices_add_exactly():
+    # the multi-GPU unit: accumulators of disjoint k-slabs sum to the full one (exact: integer data)
+    w = W.make("cfg3", xp=torch, device="cuda")
+    words = O.draw_words(w.sketch_seed, w.d, w.b)
+    at = _device.transpose(w.a)
+    full = _device.compress_accumulate(at, w.bmat, words, w.d, w.log2b, "fwht", 0, w.n)
+    world = 8
+    parts = torch.zeros_like(full)
+    for r in range(world):
+        k0, k1 = r * w.n // world, (r + 1) * w.n // world
+        parts += _device.compress_accumulate(at[k0:k1], w.bmat[k0:k1], words, w.d, w.log2b, "fwht", 0, k1 - k0)
+    assert torch.equal(parts, full)
+    # and a slab against the CPU oracle (bounded size)
+    k0, k1 = 1000, 1016
+    acc = _device.compress_accumulate(at, w.bmat, words, w.d, w.log2b, "fwht", k0, k1).cpu().numpy()
+    ref = O.accumulate_fwht(at[k0:k1].cpu().numpy(), w.bmat[k0:k1].cpu().numpy(), b=w.b, d=w.d, words=words,
+                            k0=0, k1=k1 - k0, threads=8)
+    assert np.array_equal(acc, ref)
+
+
+def test_cfg4_full_size_properties():
+    w = W.make("cfg4", xp=torch, device="cuda")
+    p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+    words = O.draw_words(p.seed, p.d, p.b)
+    at = _device.transpose(w.a)
+    cn = float(torch.linalg.norm(w.a @ w.bmat))  # ||C||_F (C = S up to rounding)
+    # k-slab vs the CPU oracle
+    k0, k1 = 4096, 4104
+    acc = _device.compress_accumulate(at, w.bmat, words, p.d, p.log2b, "fwht", k0, k1).cpu().numpy()
+    ref = O.accumulate_fwht(at[k0:k1].cpu().numpy(), w.bmat[k0:k1].cpu().numpy(), b=w.b, d=w.d, words=words,
+                            k0=0, k1=k1 - k0, threads=8)
+    assert np.max(np.abs(acc - ref)) <= 1e-12 * max(1.0, np.abs(ref).max())
+    # 8-way k-sharded accumulate == single-GPU accumulate (only the summation order differs)
+    full = _device.compress_accumulate(at, w.bmat, words, p.d, p.log2b, "fwht", 0, w.n)
+    parts = torch.zeros_like(full)
+    for r in range(8):
+        a0, a1 = r * w.n // 8, (r + 1) * w.n // 8
+        parts += _device.compress_accumulate(at[a0:a1], w.bmat[a0:a1], words, p.d, p.log2b, "fwht", 0, a1 - a0)
+    polys = _device.finalize(full, p.d, p.log2b, "fwht")
+    polys8 = _device.finalize(parts, p.d, p.log2b, "fwht")
+    assert float((polys - polys8).abs().max()) <= TOL * cn
+    sk = P.ProductSketch(polys, SketchHashes.from_words(words, p.d, p.b), p, w.n, w.n)
+    est = P.decompress_rows(sk)
+    big = torch.as_tensor(w.big, device="cuda")
+    assert float((est[big[:, 0], big[:, 1]].abs() > 0.5).float().mean()) > 0.95
+    g = cfg_golden("cfg4")
+    if g is not None:
+        samp = np.take_along_axis(sk.polys, g["polys_sample_idx"], axis=1)
+        assert np.max(np.abs(samp - g["polys_sample"])) <= TOL * cn
+        hh = P.heavy_hitters(sk, w.threshold, strict=True)
+        assert hh.shape[0] == int(g["hh_count"][0])
+        assert _sha(hh.astype(np.int64)) == bytes(g["hh_sha256"]).decode()
+
+
+def test_determinism_and_threads_independence():
+    rng = np.random.default_rng(14)
+    a, m = rng.normal(size=(96, 96)), rng.normal(size=(96, 96))
+    for tr in ("fwht", "fft"):
+        p = P.SketchParams(n=96, b=1 << 14, d=3, transform=tr, seed=15)
+        s1 = P.compress(a, m, p, threads=1).polys
+        s2 = P.compress(a, m, p, threads=5).polys
+        assert np.array_equal(s1, s2)
+
+
+def test_pretransposed_agrees_bitwise():
+    rng = np.random.default_rng(5)
+    a, m = rng.normal(size=(300, 300)), rng.normal(size=(300, 300))
+    for tr, b in (("fwht", 1 << 13), ("fwht", 1 << 16), ("fft", 1 << 12)):
+        p = P.SketchParams(n=300, b=b, d=3, transform=tr, seed=8)
+        assert np.array_equal(P.compress(a, m, p).polys, P.compress_pretransposed(np.ascontiguousarray(a.T), m, p).polys)
+
+
+def test_large_width_and_depth_against_oracle():
+    # b up to 2^20 (cfg5 range) and d = 37 (reference acceptance criterion 5 depth)
+    rng = np.random.default_rng(21)
+    for n, b, d, tr in ((256, 1 << 20, 3, "fwht"), (128, 1 << 18, 5, "fft"), (200, 512, 37, "fwht"),
+                        (200, 512, 37, "fft"), (1000, 1 << 13, 9, "fwht"), (700, 1 << 15, 1, "fwht")):
+        a, m = rng.normal(size=(n, n)), rng.normal(size=(n, n))
+        p = P.SketchParams(n=n, b=b, d=d, transform=tr, seed=31)
+        got = P.compress(a, m, p).polys
+        ref = O.compress(a, m, b=b, d=d, transform=tr, seed=31, threads=8)
+        cn = _cnorm(a, m)
+        assert np.max(np.abs(got - ref)) <= TOL * cn, (n, b, d, tr)
+        est = P.decompress_all(P.compress(a, m, p))
+        eref, _, _ = O.decompress(ref, O.draw_words(31, d, b), b=b, d=d, transform=tr, n1=n, n2=n)
+        assert np.max(np.abs(est - eref)) <= TOL * cn
+
+
+def test_heavy_hitter_comparators_and_order():
+    # polys engineered so estimates hit the threshold exactly: strict excludes, inclusive includes
+    b, d = 16, 3
+    words = np.array([1 << 60, 0] * 3 + [1 << 60, 0] * 3 + [0, 0] * 6, dtype=np.uint64)  # bucket(x)=x, sign +1
+    hashes = SketchHashes.from_words(words, d, b)
+    polys = np.tile(np.array([0.5, -0.5, 0.25, 1.0, -2.0, 0.5, 0.0, 3.0] * 2), (d, 1))
+    p = P.SketchParams(n=4, b=b, d=d, seed=0)
+    sk = P.ProductSketch(polys, hashes, p, 4, 4)
+    est = P.decompress_all(sk)
+    for strict in (True, False):
+        got = P.heavy_hitters(sk, 0.5, strict=strict)
+        _, cnt, ref = O.decompress(polys, words, b=b, d=d, transform="fwht", n1=4, n2=4, thr=0.5, strict=strict,
+                                   want_hh=True)
+        assert np.array_equal(got, ref) and got.shape[0] == cnt
+        mask = np.abs(est) > 0.5 if strict else np.abs(est) >= 0.5
+        assert np.array_equal(got, np.argwhere(mask))
+    assert P.heavy_hitters(sk, 0.5, strict=False).shape[0] > P.heavy_hitters(sk, 0.5, strict=True).shape[0]
+
+
+def test_row_sharded_extraction_matches_full():
+    rng = np.random.default_rng(3)
+    a, m = rng.normal(size=(257, 257)), rng.normal(size=(257, 257))
+    sk = P.compress(a, m, P.SketchParams(n=257, b=1 << 12, d=5, seed=2))
+    full = P.decompress_rows(sk)
+    for r0, r1 in ((0, 100), (100, 257), (37, 38), (5, 5)):
+        part = P.decompress_rows(sk, r0, r1)
+        assert torch.equal(part, full[r0:r1])
+        hh = P.heavy_hitters(sk, 1.0, r0=r0, r1=r1)
+        ref = np.argwhere(np.abs(full[r0:r1].cpu().numpy()) > 1.0)
+        ref[:, 0] += r0
+        assert np.array_equal(hh, ref)
+
+
+def test_empty_k_range_gives_zero_accumulator():
+    words = O.draw_words(1, 3, 1 << 13)
+    at = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    for tr in ("fwht", "fft"):
+        acc = _device.compress_accumulate(at, at, words, 3, 13, tr, 4, 4)
+        assert float(acc.abs().max()) == 0.0
+
+
+def test_transforms_api(transforms_golden):
+    g = transforms_golden
+    assert P.fwht_inplace(np.array([1.0, 2, 3, 4])).tolist() == [10, -2, -4, 0]
+    assert np.allclose(P.xor_convolve([1, 2], [3, 4]), [11, 10])
+    assert np.allclose(P.cyclic_convolve([1, 2], [3, 4]), [11, 10])
+    assert np.allclose(P.fft_forward([0, 1, 0, 0]), [1, -1j, -1], atol=1e-12)
+    for bstr, v in g["vectors"].items():
+        x, y = np.array(v["x"]), np.array(v["y"])
+        assert np.array_equal(P.fwht_inplace(x.copy()), np.array(v["fwht"]))
+        assert np.allclose(P.xor_convolve(x, y), v["xor"], rtol=0, atol=1e-12 * max(1, np.abs(v["xor"]).max()))
+        assert np.allclose(P.cyclic_convolve(x, y), v["cyc"], rtol=0, atol=1e-11 * max(1, np.abs(v["cyc"]).max()))
+        z = P.fft_forward(x)
+        assert np.allclose(z.real, v["fft_re"], atol=1e-11) and np.allclose(z.imag, v["fft_im"], atol=1e-11)
+    with pytest.raises(P.InvalidSpectrumError):
+        P.fft_inverse([1 + 1e-3j, 0, 1])
+    with pytest.raises(P.InvalidParameterError):
+        P.fwht_inplace(np.zeros(6))
