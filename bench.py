@@ -205,19 +205,16 @@ def run_ours(args) -> None:
     params = P.SketchParams(n=n, b=b, d=d, transform=w.transform, seed=w.sketch_seed)
     k0, k1 = shard_bounds(n, world, rank)
     r0, r1 = row_bounds(n, world, rank)
-    # this rank's device-resident inputs: the k-slab of A (columns) and of B (rows)
-    a_slab = w.a[:, k0:k1].contiguous()
-    b_slab = w.bmat[k0:k1].contiguous()
-    del w.a, w.bmat
-    torch.cuda.empty_cache()
+    # this rank's device-resident inputs: the k-slab of A (a column view, no copy) and of B (rows)
+    a_slab = w.a[:, k0:k1]
+    b_slab = w.bmat[k0:k1]
     est_buf = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
 
     def step():
         if world == 1:
-            sk = P.compress(a_slab, b_slab, params)
+            sk = P.compress(w.a, w.bmat, params)
         else:
-            at = _device.transpose(a_slab)
-            sk = compress_sharded(at, b_slab, params, n_rows=n, n_cols=n)
+            sk = compress_sharded(a_slab, b_slab, params, n_rows=n, n_cols=n, a_layout=_device.KMINOR)
         est, pairs = P.extract_all(sk, w.threshold, strict=True, r0=r0, r1=r1, est_out=est_buf)
         return sk, est, pairs
 
@@ -248,16 +245,21 @@ def run_ours(args) -> None:
 
     # ---- kernel-level timing of the dominant kernel (compress accumulate) for the roofline
     words = sk.words
-    at_full = _device.transpose(a_slab)
+    bt = b_slab.T.contiguous()  # both operands k-minor: the timed launch is plan + fwht2p_kernel only
     kl = k1 - k0
+
+    def accumulate():
+        return _device.compress_accumulate(a_slab, bt, words, d, params.log2b, "fwht", 0, kl,
+                                           a_layout=_device.KMINOR, b_layout=_device.KMINOR)
+
     for _ in range(2):
-        acc = _device.compress_accumulate(at_full, b_slab, words, d, params.log2b, "fwht", 0, kl)
+        acc = accumulate()
     torch.cuda.synchronize()
     reps = 3
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        acc = _device.compress_accumulate(at_full, b_slab, words, d, params.log2b, "fwht", 0, kl)
+        acc = accumulate()
     e1.record()
     torch.cuda.synchronize()
     t_comp = e0.elapsed_time(e1) / reps
@@ -273,7 +275,7 @@ def run_ours(args) -> None:
     ops = 2 * d * kl * b * logb + d * kl * b + 2 * d * kl * n
     achieved = ops / (t_comp * 1e-3) / 1e12
     hbm_bytes = 16 * n * kl + 8 * d * b
-    roofline = {"bound": "fp64", "kernel": "fwht_fold_kernel (smm_compress_accumulate)", "achieved": achieved,
+    roofline = {"bound": "fp64", "kernel": "fwht2p_kernel (+ CSR plan kernels) via smm_compress_accumulate_ex", "achieved": achieved,
                 "peak": FP64_PIPE_PEAK_TOPS, "unit": "Tops/s", "frac": achieved / FP64_PIPE_PEAK_TOPS,
                 "traffic": None, "algorithmic_ops": ops, "kernel_ms": t_comp,
                 "peak_source": "measured DADD pipe rate, tools/microbench.cu (profiles/r01_microbench.txt); "
@@ -293,18 +295,18 @@ def run_ours(args) -> None:
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
     if not args.no_e2e:
-        a_host = a_slab.cpu().pin_memory()
-        b_host = b_slab.cpu().pin_memory()
+        a_host = a_slab.contiguous().cpu().pin_memory()
+        b_host = b_slab.contiguous().cpu().pin_memory()
         est_host = torch.empty((r1 - r0, n), dtype=torch.float64).pin_memory()
-        del at_full, acc
+        del bt, acc
         torch.cuda.empty_cache()
 
         def e2e_step():
             if world == 1:
                 sk2 = P.compress(a_host, b_host, params)
             else:
-                at = _device.transpose(a_host.to(dev, non_blocking=True))
-                sk2 = compress_sharded(at, b_host.to(dev, non_blocking=True), params, n_rows=n, n_cols=n)
+                sk2 = compress_sharded(a_host.to(dev, non_blocking=True), b_host.to(dev, non_blocking=True), params,
+                                       n_rows=n, n_cols=n, a_layout=_device.KMINOR)
             est2, pairs2 = P.extract_all(sk2, w.threshold, strict=True, r0=r0, r1=r1, est_out=est_buf)
             est_host.copy_(est2, non_blocking=True)
             return pairs2.to("cpu")

@@ -49,6 +49,9 @@ extern "C" {
 
 #define SMM_MAX_DEPTH 63
 
+#define SMM_LAYOUT_KMAJOR 0
+#define SMM_LAYOUT_KMINOR 1
+
 int smm_abi_version(void);
 const char *smm_last_error(void);
 
@@ -73,6 +76,20 @@ int smm_compress_accumulate(int variant, const double *at, int64_t ld_at, const 
                             int64_t ld_bm, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
                             const uint64_t *words_host, int d, int log2b, void *acc,
                             void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Same as smm_compress_accumulate with explicit operand layouts:
+ *   SMM_LAYOUT_KMAJOR: row k holds inner index k (the reference's `at` = A^T and B);
+ *   SMM_LAYOUT_KMINOR: row i holds element i, inner index k contiguous (A row-major,
+ *                      B^T row-major) — the layout the two-pass FWHT kernel reads.
+ * lda/ldb are leading dimensions in that layout.  The library transposes the
+ * [k0, k1) slab of an operand whose layout differs from what the selected kernel
+ * reads into the workspace (size from smm_compress_workspace_ex). */
+int smm_compress_workspace_ex(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0,
+                              int64_t k1, int a_layout, int b_layout, int64_t *bytes);
+int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_layout,
+                               const double *b, int64_t ldb, int b_layout, int64_t n1, int64_t n2,
+                               int64_t k0, int64_t k1, const uint64_t *words_host, int d, int log2b,
+                               void *acc, void *workspace, int64_t workspace_bytes, void *stream);
 
 /* Step 4: polys [dev] (d x b float64) = inverse transform of acc, times 1/b. */
 int smm_finalize(int variant, const void *acc, double *polys, int d, int log2b, void *stream);

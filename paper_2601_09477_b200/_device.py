@@ -83,22 +83,42 @@ def acc_shape(variant: str, d: int, b: int):
     return (d, b) if variant == "fwht" else (d, b // 2 + 1, 2)
 
 
-def compress_accumulate(at: torch.Tensor, bm: torch.Tensor, words: np.ndarray, d: int, log2b: int,
-                        variant: str, k0: int, k1: int, acc: torch.Tensor | None = None) -> torch.Tensor:
-    """Pre-inverse accumulator of inner indices [k0, k1) (rows of at / bm)."""
+KMAJOR = 0  # row k holds inner index k (the reference's A^T and B)
+KMINOR = 1  # row i holds element i, inner index contiguous (A row-major, B^T row-major)
+
+
+def _rowmajor(x: torch.Tensor) -> torch.Tensor:
+    if x.dim() != 2 or x.dtype != torch.float64 or not x.is_cuda:
+        raise InvalidParameterError("operands must be 2-D float64 CUDA tensors")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    return x
+
+
+def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str,
+                        k0: int, k1: int, acc: torch.Tensor | None = None, a_layout: int = KMAJOR,
+                        b_layout: int = KMAJOR) -> torch.Tensor:
+    """Pre-inverse accumulator of inner indices [k0, k1).
+
+    ``a`` is A^T (KMAJOR, rows = k) or A itself (KMINOR, columns = k); ``b`` is B
+    (KMAJOR) or B^T (KMINOR).  Views with a row stride are used in place.
+    """
     lib = _lib.load()
-    dev = at.device
-    n1 = at.shape[1]
-    n2 = bm.shape[1]
+    a = _rowmajor(a)
+    b = _rowmajor(b)
+    dev = a.device
+    n1 = a.shape[1] if a_layout == KMAJOR else a.shape[0]
+    n2 = b.shape[1] if b_layout == KMAJOR else b.shape[0]
     v = _lib.VARIANT[variant]
     nbytes = ctypes.c_int64(0)
-    _lib.check(lib.smm_compress_workspace(v, d, log2b, n1, n2, k0, k1, ctypes.byref(nbytes)))
+    _lib.check(lib.smm_compress_workspace_ex(v, d, log2b, n1, n2, k0, k1, a_layout, b_layout, ctypes.byref(nbytes)))
     ws = workspace(nbytes.value, dev)
     if acc is None:
         acc = torch.empty(acc_shape(variant, d, 1 << log2b), dtype=torch.float64, device=dev)
     words, wp = words_ptr(words)
-    _lib.check(lib.smm_compress_accumulate(v, ptr(at), at.stride(0), ptr(bm), bm.stride(0), n1, n2, k0, k1, wp, d,
-                                           log2b, ptr(acc), ptr(ws), ws.numel(), stream_ptr(dev)))
+    _lib.check(lib.smm_compress_accumulate_ex(v, ptr(a), a.stride(0), a_layout, ptr(b), b.stride(0), b_layout, n1,
+                                              n2, k0, k1, wp, d, log2b, ptr(acc), ptr(ws), ws.numel(),
+                                              stream_ptr(dev)))
     return acc
 
 

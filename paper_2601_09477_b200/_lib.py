@@ -28,6 +28,8 @@ EXPORTS = (
     "smm_hash_tables",
     "smm_compress_workspace",
     "smm_compress_accumulate",
+    "smm_compress_workspace_ex",
+    "smm_compress_accumulate_ex",
     "smm_finalize",
     "smm_extract_workspace",
     "smm_extract",
@@ -70,6 +72,8 @@ def load():
             "smm_hash_tables": ([P, I, I, I, I64, P, P, P], I),
             "smm_compress_workspace": ([I, I, I, I64, I64, I64, I64, P], I),
             "smm_compress_accumulate": ([I, P, I64, P, I64, I64, I64, I64, I64, P, I, I, P, P, I64, P], I),
+            "smm_compress_workspace_ex": ([I, I, I, I64, I64, I64, I64, I, I, P], I),
+            "smm_compress_accumulate_ex": ([I, P, I64, I, P, I64, I, I64, I64, I64, I64, P, I, I, P, P, I64, P], I),
             "smm_finalize": ([I, P, P, I, I, P], I),
             "smm_extract_workspace": ([I, I64, I64, I64, I64, P], I),
             "smm_extract": ([I, P, P, I, I, I64, I64, I64, I64, P, I64, D, I, P, I64, P, P, I64, P], I),

@@ -8,6 +8,11 @@ const char *last_error();
 int hash_tables(const SketchHashes &h, int group, int64_t n, uint32_t *buckets, int8_t *signs, cudaStream_t s);
 int64_t fwht_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K, int G);
 int64_t fft_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K, int Gmax);
+bool fwht2p_supported(int log2b, int64_t n1, int64_t n2);
+int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K);
+int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb,
+                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
+                      cudaStream_t s);
 int fwht_accumulate(const SketchHashes &h, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm,
                     int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
                     cudaStream_t s);
@@ -66,35 +71,113 @@ int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int
   return hash_tables(h, group, n, buckets_out, signs_out, (cudaStream_t)stream);
 }
 
-int smm_compress_workspace(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
-                           int64_t *bytes) {
+// ---------------------------------------------------------------- compress dispatch
+// The two-pass FWHT kernel reads k-minor operands (row = input index, k
+// contiguous); the fold kernels (FFT, small/large b) read k-major rows.  An
+// operand in the other layout is transposed (only its [k0, k1) slab) into the
+// front of the workspace.
+struct CompressPlan {
+  bool two_pass;
+  bool ta, tb;  // transpose A / B slab
+  int64_t ta_bytes, tb_bytes, kernel_bytes;
+};
+
+static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t K, int alay,
+                                  int blay) {
+  CompressPlan c;
+  c.two_pass = variant == SMM_VARIANT_FWHT && fwht2p_supported(log2b, n1, n2);
+  const int want = c.two_pass ? SMM_LAYOUT_KMINOR : SMM_LAYOUT_KMAJOR;
+  c.ta = alay != want;
+  c.tb = blay != want;
+  c.ta_bytes = c.ta ? ((n1 * K * 8 + 255) / 256) * 256 : 0;
+  c.tb_bytes = c.tb ? ((n2 * K * 8 + 255) / 256) * 256 : 0;
+  if (c.two_pass) c.kernel_bytes = fwht2p_workspace(d, log2b, n1, n2, K);
+  else if (variant == SMM_VARIANT_FWHT) c.kernel_bytes = fwht_workspace(d, log2b, n1, n2, K, num_sms());
+  else c.kernel_bytes = fft_workspace(d, log2b, n1, n2, K, num_sms());
+  return c;
+}
+
+int smm_compress_workspace_ex(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
+                              int a_layout, int b_layout, int64_t *bytes) {
   int rc = check_sketch(variant, d, log2b);
   if (rc) return rc;
   SMM_REQUIRE(bytes != nullptr, "bytes is NULL");
   SMM_REQUIRE(n1 >= 0 && n2 >= 0 && k0 >= 0 && k1 >= k0, "bad shapes");
-  *bytes = variant == SMM_VARIANT_FWHT ? fwht_workspace(d, log2b, n1, n2, k1 - k0, num_sms())
-                                       : fft_workspace(d, log2b, n1, n2, k1 - k0, num_sms());
+  SMM_REQUIRE((a_layout == 0 || a_layout == 1) && (b_layout == 0 || b_layout == 1), "bad layout");
+  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, k1 - k0, a_layout, b_layout);
+  *bytes = c.ta_bytes + c.tb_bytes + c.kernel_bytes;
   return SMM_OK;
 }
 
-int smm_compress_accumulate(int variant, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm, int64_t n1,
-                            int64_t n2, int64_t k0, int64_t k1, const uint64_t *words_host, int d, int log2b,
-                            void *acc, void *workspace, int64_t workspace_bytes, void *stream) {
+int smm_compress_workspace(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
+                           int64_t *bytes) {
+  return smm_compress_workspace_ex(variant, d, log2b, n1, n2, k0, k1, SMM_LAYOUT_KMAJOR, SMM_LAYOUT_KMAJOR, bytes);
+}
+
+int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_layout, const double *b, int64_t ldb,
+                               int b_layout, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
+                               const uint64_t *words_host, int d, int log2b, void *acc, void *workspace,
+                               int64_t workspace_bytes, void *stream) {
   int rc = check_sketch(variant, d, log2b);
   if (rc) return rc;
   SMM_REQUIRE(words_host != nullptr && acc != nullptr, "NULL argument");
   SMM_REQUIRE(n1 >= 0 && n2 >= 0 && n1 < ((int64_t)1 << 31) && n2 < ((int64_t)1 << 31), "operand sizes out of range");
   SMM_REQUIRE(k0 >= 0 && k1 >= k0, "inner range [%lld, %lld) invalid", (long long)k0, (long long)k1);
-  SMM_REQUIRE(k1 == k0 || ((at != nullptr || n1 == 0) && (bm != nullptr || n2 == 0)), "operand pointer is NULL");
-  SMM_REQUIRE(ld_at >= n1 && ld_bm >= n2, "leading dimension smaller than row length");
+  SMM_REQUIRE((a_layout == 0 || a_layout == 1) && (b_layout == 0 || b_layout == 1), "bad layout");
+  SMM_REQUIRE(k1 == k0 || ((a != nullptr || n1 == 0) && (b != nullptr || n2 == 0)), "operand pointer is NULL");
+  SMM_REQUIRE(a_layout == SMM_LAYOUT_KMAJOR ? lda >= n1 : lda >= k1, "lda too small for the layout");
+  SMM_REQUIRE(b_layout == SMM_LAYOUT_KMAJOR ? ldb >= n2 : ldb >= k1, "ldb too small for the layout");
   SketchHashes h;
   load_hashes(h, words_host, d, log2b);
   cudaStream_t s = (cudaStream_t)stream;
+  const int64_t K = k1 - k0;
+  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, K, a_layout, b_layout);
+  if (workspace_bytes < c.ta_bytes + c.tb_bytes + c.kernel_bytes) {
+    set_error("compress workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
+              (long long)(c.ta_bytes + c.tb_bytes + c.kernel_bytes));
+    return SMM_ERR_WORKSPACE;
+  }
+  char *ws = (char *)workspace;
+  // operand views in the layout the chosen kernel reads; offsets so that inner index k0 maps to x[.. + k0]
+  const double *xa = a, *xb = b;
+  int64_t la = lda, lb = ldb, kk0 = k0, kk1 = k1;
+  if (c.ta || c.tb) { kk0 = 0; kk1 = K; }
+  if (!(c.ta || c.tb)) {
+    // no copies: kernels index with k0 directly
+  } else {
+    // both operands must share the same k origin: shift the untouched one to its slab
+    if (!c.ta) xa = c.two_pass ? a + k0 : a + k0 * lda;
+    if (!c.tb) xb = c.two_pass ? b + k0 : b + k0 * ldb;
+  }
+  if (c.ta) {
+    double *t = (double *)ws;
+    if (a_layout == SMM_LAYOUT_KMAJOR) rc = transpose(a + k0 * lda, K, n1, lda, t, K, s);  // -> n1 x K
+    else rc = transpose(a + k0, n1, K, lda, t, n1, s);                                      // -> K x n1
+    if (rc) return rc;
+    xa = t;
+    la = c.two_pass ? K : n1;
+  }
+  if (c.tb) {
+    double *t = (double *)(ws + c.ta_bytes);
+    if (b_layout == SMM_LAYOUT_KMAJOR) rc = transpose(b + k0 * ldb, K, n2, ldb, t, K, s);  // -> n2 x K
+    else rc = transpose(b + k0, n2, K, ldb, t, n2, s);                                      // -> K x n2
+    if (rc) return rc;
+    xb = t;
+    lb = c.two_pass ? K : n2;
+  }
+  char *kws = ws + c.ta_bytes + c.tb_bytes;
+  const int64_t kb = workspace_bytes - c.ta_bytes - c.tb_bytes;
+  if (c.two_pass) return fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, kws, kb, s);
   if (variant == SMM_VARIANT_FWHT)
-    return fwht_accumulate(h, at, ld_at, bm, ld_bm, n1, n2, k0, k1, (double *)acc, (char *)workspace,
-                           workspace_bytes, s);
-  return fft_accumulate(h, at, ld_at, bm, ld_bm, n1, n2, k0, k1, (cplx *)acc, (char *)workspace, workspace_bytes,
-                        s);
+    return fwht_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, kws, kb, s);
+  return fft_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (cplx *)acc, kws, kb, s);
+}
+
+int smm_compress_accumulate(int variant, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm, int64_t n1,
+                            int64_t n2, int64_t k0, int64_t k1, const uint64_t *words_host, int d, int log2b,
+                            void *acc, void *workspace, int64_t workspace_bytes, void *stream) {
+  return smm_compress_accumulate_ex(variant, at, ld_at, SMM_LAYOUT_KMAJOR, bm, ld_bm, SMM_LAYOUT_KMAJOR, n1, n2, k0, k1,
+                                    words_host, d, log2b, acc, workspace, workspace_bytes, stream);
 }
 
 int smm_finalize(int variant, const void *acc, double *polys, int d, int log2b, void *stream) {

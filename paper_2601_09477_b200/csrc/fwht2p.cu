@@ -1,0 +1,611 @@
+// FWHT compress v2 (steps 1-3) for 2^9 <= b <= 2^16: two-pass, persistent,
+// dependency-ordered.  Reference: sketch.py:152-189, transforms.py:37-49.
+//
+// Why two passes.  A length-b FP64 transform does log2(b) adds per element;
+// on B200 the FP64 pipe retires 64 adds/clk/SM while shared memory moves 16
+// doubles/clk/SM, so every on-chip element exchange costs as much as ~8 FWHT
+// stages and a random-access scatter costs ~3x more.  This kernel therefore
+// (1) makes the scatter a *coalesced* pull: lanes carry 32 consecutive inner
+// indices k, so each input element i contributes one 256-byte row segment
+// X[i, k0:k0+32] of the k-minor operand (A row-major, B^T row-major); (2)
+// keeps bucket bits in registers (5 stages free), moves 4 more bits through
+// ONE shared-memory exchange (pass 1, 9 low bits) and up to 2 more through a
+// tensor-memory (TMEM) exchange (pass 2, high bits) — TMEM ld/st run at
+// 177/400 B/clk/SM on a datapath separate from shared memory; (3) parks the
+// pass-1 result Y (b x 32 doubles per repetition and operand) in the 126 MB
+// L2 between the passes, in a 3-slot ring; (4) accumulates FA*FB over k in
+// registers (lane reduction) and adds it to the d x b accumulator once per
+// k-tile.
+//
+// Scheduling: one persistent CTA per SM pulls tickets from a global counter in
+// a fixed order [P1(0)] [P1(1) P2(0)] [P1(2) P2(1)] ... where a unit u is
+// (k-tile kappa = u / d, repetition t = u % d).  Every item's dependencies
+// (P2(u) needs all P1(u); P1(u) reuses the Y slot of P2(u-3); P2(kappa, t, s)
+// extends the accumulator after P2(kappa-1, t, s)) are dispensed earlier, so
+// spinning on them cannot deadlock; accumulator updates happen in k order, so
+// results are bit-reproducible.
+#include "plan.cuh"
+
+namespace smm {
+
+constexpr int P_THREADS = 512;
+constexpr int KT = 32;
+constexpr int P1_BITS = 9;
+
+// ------------------------------------------------------------------ CSR plan
+// entries sorted by (bucket, i) per (t, op): off [d][2][b+1], ent [d][2][nmax] = i | sign << 31
+__global__ void csr_count_kernel(SketchHashes h, int64_t n1, int64_t n2, int32_t *cnt, int64_t b) {
+  const int64_t per = n1 + n2;
+  const int64_t total = (int64_t)h.d * per;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x / per);
+    const int64_t q = x % per;
+    const int op = q < n1 ? 0 : 1;
+    const int64_t i = op ? q - n1 : q;
+    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b);
+    atomicAdd(&cnt[((int64_t)t * 2 + op) * b + m], 1);
+  }
+}
+
+__global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b) {
+  __shared__ int32_t s[1024];
+  __shared__ int32_t carry;
+  const int64_t row = blockIdx.x;  // (t, op)
+  const int32_t *c = cnt + row * b;
+  int32_t *o = off + row * (b + 1);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < b; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < b ? c[i] : 0;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+      int32_t add = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
+      __syncthreads();
+      s[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < b) o[i] = carry + s[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) o[b] = carry;
+}
+
+__global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const int32_t *off, int32_t *fill,
+                                uint32_t *ent, int64_t nmax, int64_t b) {
+  const int64_t per = n1 + n2;
+  const int64_t total = (int64_t)h.d * per;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x / per);
+    const int64_t q = x % per;
+    const int op = q < n1 ? 0 : 1;
+    const int64_t i = op ? q - n1 : q;
+    const int64_t row = (int64_t)t * 2 + op;
+    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b);
+    const uint32_t sb = eval_signbit(h.f[2 + op][t], (uint64_t)i);
+    const int32_t pos = off[row * (b + 1) + m] + atomicAdd(&fill[row * b + m], 1);
+    ent[row * nmax + pos] = (uint32_t)i | (sb << 31);
+  }
+}
+
+// deterministic order inside each bucket: increasing i (the reference's serial order)
+__global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows) {
+  const int64_t total = (int64_t)rows * b;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = x / b, m = x % b;
+    const int32_t e0 = off[row * (b + 1) + m], e1 = off[row * (b + 1) + m + 1];
+    uint32_t *e = ent + row * nmax;
+    for (int32_t a = e0 + 1; a < e1; ++a) {
+      const uint32_t key = e[a];
+      int32_t q = a - 1;
+      while (q >= e0 && (e[q] & 0x7fffffffu) > (key & 0x7fffffffu)) {
+        e[q + 1] = e[q];
+        --q;
+      }
+      e[q + 1] = key;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+struct TwoPassArgs {
+  SketchHashes h;
+  const double *X[2];  // k-minor operands: element (i, k) at X[op][i * ld[op] + k]
+  int64_t ld[2];
+  int64_t k0, K;
+  int B, hb, d, nblk, ntiles, U, nslot;
+  const int32_t *off;
+  const uint32_t *ent;
+  int64_t nmax, bsz;
+  double *Y;   // [nslot][2][b][KT]
+  double *acc; // [d][b]
+  int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
+};
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_geq(const int *p, int target) {
+  if (ld_acquire(p) >= target) return;
+  while (ld_acquire(p) < target) __nanosleep(64);
+}
+
+// ---- TMEM helpers (32x32b shape: thread <-> TMEM lane, 16 x 32-bit columns = 8 doubles)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const double *v) {
+  uint32_t r[16];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    r[2 * q] = (uint32_t)__double2loint(v[q]);
+    r[2 * q + 1] = (uint32_t)__double2hiint(v[q]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, double *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __hiloint2double((int)r[2 * q + 1], (int)r[2 * q]);
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// L2 cache-policy hints: Y (the pass-1 -> pass-2 intermediate) is written
+// evict_last so it survives in L2 until pass 2, and read evict_first (last use).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_hint(double *p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_hint(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+
+// in-register butterflies over register-index bits [qlo, qhi)
+__device__ __forceinline__ void reg_fwht32(double (&v)[32], int qlo, int qhi) {
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    if (q >= qlo && q < qhi) {
+      const int h = 1 << q;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (!(j & h)) {
+          const double x = v[j], y = v[j + h];
+          v[j] = x + y;
+          v[j + h] = x - y;
+        }
+      }
+    }
+  }
+}
+
+#define SMM_CASE(J) \
+  case J:           \
+    v[J] += val;    \
+    break;
+
+// Pass 1: pull the 512 buckets [blk*512, blk*512+512) of operand op for the
+// 32 inner indices of k-tile kappa, FWHT over the 9 low bucket bits, write Y.
+__device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, int blk, double *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kappa = u / p.d, t = u % p.d;
+  const bool kvalid = (int64_t)kappa * KT + lane < p.K;
+  const double *X = p.X[op] + (p.k0 + (int64_t)kappa * KT + lane);
+  const int64_t ld = p.ld[op];
+  const int64_t base = (int64_t)blk * 512 + warp * 32;
+  const int64_t row = (int64_t)t * 2 + op;
+  const int32_t *off = p.off + row * (p.bsz + 1);
+  const uint32_t *ent = p.ent + row * p.nmax;
+  const HashFn hf = p.h.f[op][t];
+  const int e_lo = off[base];
+  const int e_hi = off[base + 32];
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.0;
+  for (int eb = e_lo; eb < e_hi; eb += 8) {
+    const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
+    uint32_t es[8];
+    double x[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      x[s] = (eb + s < e_hi && kvalid) ? __ldg(X + (int64_t)(es[s] & 0x7fffffffu) * ld) : 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (eb + s < e_hi) {  // warp-uniform
+        const uint32_t i = es[s] & 0x7fffffffu;
+        const int j = (int)((int64_t)eval_bucket(hf, (uint64_t)i, p.B) - base);
+        const double val = (es[s] >> 31) ? -x[s] : x[s];
+        switch (j) {
+          SMM_CASE(0) SMM_CASE(1) SMM_CASE(2) SMM_CASE(3) SMM_CASE(4) SMM_CASE(5) SMM_CASE(6) SMM_CASE(7)
+          SMM_CASE(8) SMM_CASE(9) SMM_CASE(10) SMM_CASE(11) SMM_CASE(12) SMM_CASE(13) SMM_CASE(14) SMM_CASE(15)
+          SMM_CASE(16) SMM_CASE(17) SMM_CASE(18) SMM_CASE(19) SMM_CASE(20) SMM_CASE(21) SMM_CASE(22) SMM_CASE(23)
+          SMM_CASE(24) SMM_CASE(25) SMM_CASE(26) SMM_CASE(27) SMM_CASE(28) SMM_CASE(29) SMM_CASE(30) SMM_CASE(31)
+          default: break;
+        }
+      }
+    }
+  }
+  reg_fwht32(v, 0, 5);  // bucket bits 0-4
+  // exchange: warp bits (bucket bits 5-8) <-> register bits 0-3
+#pragma unroll
+  for (int j = 0; j < 32; ++j) S[(warp * 32 + j) * 32 + lane] = v[j];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = S[((r & 15) * 32 + (warp + 16 * (r >> 4))) * 32 + lane];
+  reg_fwht32(v, 0, 4);  // bucket bits 5-8
+  double *Yd = p.Y + (((int64_t)(u % p.nslot) * 2 + op) * p.bsz + (int64_t)blk * 512) * KT + lane;
+  const uint64_t pol = policy_evict_last();
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const int bl = (warp + 16 * (r >> 4)) + 32 * (r & 15);
+    st_hint(Yd + (int64_t)bl * KT, v[r], pol);
+  }
+}
+
+__device__ __forceinline__ void p1_item(const TwoPassArgs &p, int u, int blk, double *S) {
+#pragma unroll 1
+  for (int op = 0; op < 2; ++op) {
+    if (op == 1) __syncthreads();  // every warp has read operand 0's exchange data from S
+    p1_operand(p, u, op, blk, S);
+  }
+}
+
+// Pass 2: for slice s (512 buckets: every high-bit value x 2^(9-hb) low values)
+// finish the transform of both operands over the hb high bits, multiply, sum
+// over the 32 inner indices and extend the accumulator.
+template <int HB>
+__device__ __forceinline__ void p2_item(const TwoPassArgs &p, int u, int s, uint32_t tmem, const int *acc_flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the accumulator of (t, s) must already hold k-tiles < kappa: poll early, check before the update
+  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
+  const int wq = warp & 3, wh = warp >> 2;
+  const int kappa = u / p.d, t = u % p.d;
+  constexpr int hb = HB;
+  const int hmask = (1 << hb) - 1;
+  const int64_t lo0 = (int64_t)s << (P1_BITS - hb);
+  // this lane's accumulator bucket after the lane reduction (fixed by the mapping)
+  const int sg_acc = hb > 5 ? ((lane & 7) | (wh << 3) | ((lane >> 3) << 5) | (wq << 7)) : (lane | (wh << 5) | (wq << 7));
+  double *a = p.acc + (int64_t)t * p.bsz + (int64_t)(sg_acc & hmask) * 512 + lo0 + (sg_acc >> hb);
+  // usually the previous k-tile's update of this slice finished long ago: fetch the old value early
+  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
+  const double acc_old = (kappa > 0 && acc_ready) ? __ldcg(a) : 0.0;
+  const uint32_t tq = tmem + ((uint32_t)(32 * wq) << 16);
+  const uint32_t col_fa = (uint32_t)(wh * 64), col_x = (uint32_t)(256 + wh * 64);
+  double v[32];
+  const uint64_t pol = policy_evict_first();
+  for (int op = 0; op < 2; ++op) {
+    const double *Ys = p.Y + ((int64_t)(u % p.nslot) * 2 + op) * p.bsz * KT + lane;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int sg = r | (wh << 5) | (wq << 7);
+      const int64_t bucket = (int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb);
+      v[r] = ld_hint(Ys + bucket * KT, pol);
+    }
+    reg_fwht32(v, 0, hb < 5 ? hb : 5);
+    // last use of these Y rows: drop the L2 lines without write-back
+    __syncwarp();
+    if ((lane & 15) == 0) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int sg = r | (wh << 5) | (wq << 7);
+        const int64_t bucket = (int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb);
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(Ys + bucket * KT) : "memory");
+      }
+    }
+    if (hb > 5) {
+      // TMEM exchange: register bits 3,4 <-> warp bits wh (slice bits 5,6), among quadrant-mates
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st8(tq + col_x + 16 * c, v + 8 * c);
+      tmem_wait_st();
+      tc_fence_before();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + wq) : "memory");  // the 4 quadrant-mate warps
+      tc_fence_after();
+#pragma unroll
+      for (int src = 0; src < 4; ++src) tmem_ld8(tq + (uint32_t)(256 + src * 64 + 16 * wh), v + 8 * src);
+      reg_fwht32(v, 3, 3 + (hb - 5));
+      tc_fence_before();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + wq) : "memory");  // exchange area is reused by the next operand
+      tc_fence_after();
+    }
+    if (op == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st8(tq + col_fa + 16 * c, v + 8 * c);
+      tmem_wait_st();
+    }
+  }
+  // product FA * FB (FB in v)
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double fa[8];
+    tmem_ld8(tq + col_fa + 16 * c, fa);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
+  }
+  // sum over the 32 inner indices (lanes): transpose-reduce, lane l ends with register l
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int r = 0; r < m; ++r) {
+      const double send = upper ? v[r] : v[r + m];
+      const double keep = upper ? v[r + m] : v[r];
+      v[r] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  if (kappa == 0) {
+    __stcg(a, v[0]);
+  } else if (acc_ready) {
+    __stcg(a, acc_old + v[0]);
+  } else {
+    if (lane == 0)
+      while (flag < kappa) {
+        __nanosleep(32);
+        flag = ld_relaxed(acc_flag);
+      }
+    __syncwarp();
+    __stcg(a, __ldcg(a) + v[0]);
+  }
+}
+
+struct Item {
+  int64_t pos;
+  int is_p1, u, idx;
+};
+
+__device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos) {
+  const int G1 = p.nblk, G2 = p.nblk;
+  Item it;
+  it.pos = pos;
+  if (pos < G1) {
+    it.is_p1 = 1; it.u = 0; it.idx = (int)pos;
+    return it;
+  }
+  const int q = (int)(pos - G1);
+  const int regular = (p.U - 1) * (G1 + G2);
+  if (q < regular) {
+    const unsigned g = (unsigned)q / (unsigned)(G1 + G2);
+    const int r = q - (int)g * (G1 + G2);
+    if (r < G1) { it.is_p1 = 1; it.u = g + 1; it.idx = r; }
+    else { it.is_p1 = 0; it.u = g; it.idx = r - G1; }
+  } else {
+    it.is_p1 = 0; it.u = p.U - 1; it.idx = (int)(q - regular);
+  }
+  return it;
+}
+
+__device__ __forceinline__ void red_release_add(int *ptr, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+
+template <int HB>
+__global__ void __launch_bounds__(P_THREADS, 1) fwht2p_kernel(TwoPassArgs p) {
+  extern __shared__ __align__(16) double S[];  // 16 warps x 32 x 32 doubles = 128 KB
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_item[4];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  int *ticket = p.ctr;
+  int *done1 = p.ctr + 1;
+  int *done2 = done1 + p.U;
+  int *acc_cnt = done2 + p.U;
+  const int G1 = p.nblk, G2 = p.nblk;  // P1 items: one block, both operands; P2 items: one slice
+  const int64_t total = (int64_t)p.U * (G1 + G2);
+  // thread 0 owns the scheduling state: the current ticket and one prefetched ticket
+  int64_t cur = 0, nxt = 0;
+  int ver1 = -1, ver2 = -1;  // units whose P1 / P2 items are all known complete (prefix)
+  if (tid == 0) {
+    cur = atomicAdd(ticket, 1);
+    nxt = atomicAdd(ticket, 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  while (true) {
+    if (tid == 0) {
+      Item it = decode_item(p, cur);
+      if (cur < total) {
+        // dependencies (dispensed earlier, so this cannot deadlock); acquire orders the reads below
+        if (it.is_p1) {
+          for (; ver2 < it.u - p.nslot; ++ver2) wait_geq(done2 + ver2 + 1, G2);
+        } else {
+          for (; ver1 < it.u; ++ver1) wait_geq(done1 + ver1 + 1, G1);
+        }
+      }
+      s_item[0] = cur < total ? 1 : 0;
+      s_item[1] = it.is_p1;
+      s_item[2] = it.u;
+      s_item[3] = it.idx;
+    }
+    __syncthreads();  // [A]
+    if (!s_item[0]) break;
+    const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
+    if (tid == 0) {
+      // prefetch the ticket after next now; its round trip overlaps this item's work
+      cur = nxt;
+      nxt = (nxt < total) ? (int64_t)atomicAdd(ticket, 1) : nxt;
+    }
+    if (is_p1) p1_item(p, u, idx, S);
+    else p2_item<HB>(p, u, idx, tmem, acc_cnt + (u % p.d) * p.nblk + idx);
+    tc_fence_before();
+    __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
+    tc_fence_after();
+    if (tid == 0) {
+      if (is_p1) red_release_add(done1 + u, 1);
+      else {
+        red_release_add(acc_cnt + (u % p.d) * p.nblk + idx, 1);
+        red_release_add(done2 + u, 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------ host
+static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
+
+bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
+  return log2b >= P1_BITS && log2b <= P1_BITS + 7 && n1 < ((int64_t)1 << 31) && n2 < ((int64_t)1 << 31);
+}
+
+static int nslots_for(int log2b) {
+  const int64_t yunit = (int64_t)2 * ((int64_t)1 << log2b) * KT * 8;
+  return yunit * 3 <= ((int64_t)100 << 20) ? 3 : 3;
+}
+
+int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
+  const int64_t b = (int64_t)1 << log2b;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  const int64_t ntiles = (K + KT - 1) / KT;
+  const int64_t U = ntiles * d;
+  const int64_t nblk = b >> P1_BITS;
+  int64_t w = 0;
+  w += pad256((int64_t)d * 2 * (b + 1) * 4);  // off
+  w += pad256((int64_t)d * 2 * b * 4);        // cnt / fill
+  w += pad256((int64_t)d * 2 * nmax * 4);     // ent
+  w += pad256((int64_t)nslots_for(log2b) * 2 * b * KT * 8);  // Y ring
+  w += pad256((1 + 2 * U + (int64_t)d * nblk) * 4);          // counters
+  return w;
+}
+
+int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb,
+                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
+                      cudaStream_t s) {
+  const int d = h.d, log2b = h.log2b;
+  const int64_t b = (int64_t)1 << log2b;
+  const int64_t K = k1 - k0;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  if (ws_bytes < fwht2p_workspace(d, log2b, n1, n2, K)) {
+    set_error("compress workspace too small (two-pass)");
+    return SMM_ERR_WORKSPACE;
+  }
+  char *q = ws;
+  int32_t *off = (int32_t *)q;
+  q += pad256((int64_t)d * 2 * (b + 1) * 4);
+  int32_t *cnt = (int32_t *)q;
+  q += pad256((int64_t)d * 2 * b * 4);
+  uint32_t *ent = (uint32_t *)q;
+  q += pad256((int64_t)d * 2 * nmax * 4);
+  double *Y = (double *)q;
+  const int nslot = nslots_for(log2b);
+  q += pad256((int64_t)nslot * 2 * b * KT * 8);
+  int *ctr = (int *)q;
+  const int64_t ntiles = (K + KT - 1) / KT;
+  const int64_t U = ntiles * d;
+  const int nblk = (int)(b >> P1_BITS);
+  if (K <= 0) {
+    SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
+    return SMM_OK;
+  }
+  if (U > (int64_t)1 << 30) {
+    set_error("inner range too large for one call");
+    return SMM_ERR_INVALID;
+  }
+  // plan (CSR by bucket)
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  const int64_t nin = (int64_t)d * (n1 + n2);
+  int64_t blocks = ceil_div(nin, 256);
+  if (blocks > 8192) blocks = 8192;
+  if (nin > 0) {
+    csr_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, b);
+    SMM_LAUNCH_CHECK("csr_count_kernel");
+  }
+  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, b);
+  SMM_LAUNCH_CHECK("csr_scan_kernel");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  if (nin > 0) {
+    csr_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, b);
+    SMM_LAUNCH_CHECK("csr_fill_kernel");
+    int64_t sb = ceil_div((int64_t)d * 2 * b, 256);
+    if (sb > 8192) sb = 8192;
+    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, b, d * 2);
+    SMM_LAUNCH_CHECK("csr_sort_kernel");
+  }
+  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * nblk) * 4, s), "counter memset");
+  TwoPassArgs p;
+  p.h = h;
+  p.X[0] = xa;
+  p.X[1] = xb;
+  p.ld[0] = lda;
+  p.ld[1] = ldb;
+  p.k0 = k0;
+  p.K = K;
+  p.B = log2b;
+  p.hb = log2b - P1_BITS;
+  p.d = d;
+  p.nblk = nblk;
+  p.ntiles = (int)ntiles;
+  p.U = (int)U;
+  p.nslot = nslot;
+  p.off = off;
+  p.ent = ent;
+  p.nmax = nmax;
+  p.bsz = b;
+  p.Y = Y;
+  p.acc = acc;
+  p.ctr = ctr;
+  const size_t smem = (size_t)16 * 32 * 32 * 8;
+  // one persistent CTA per SM (TMEM is fully allocated per CTA, so co-residency is exactly 1)
+  const int G = num_sms();
+  switch (p.hb) {
+#define SMM_LAUNCH_HB(H)                                                                                 \
+  case H:                                                                                                \
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+                 "fwht2p smem");                                                                         \
+    fwht2p_kernel<H><<<G, P_THREADS, smem, s>>>(p);                                                      \
+    break;
+    SMM_LAUNCH_HB(0) SMM_LAUNCH_HB(1) SMM_LAUNCH_HB(2) SMM_LAUNCH_HB(3)
+    SMM_LAUNCH_HB(4) SMM_LAUNCH_HB(5) SMM_LAUNCH_HB(6) SMM_LAUNCH_HB(7)
+#undef SMM_LAUNCH_HB
+    default:
+      set_error("two-pass kernel: unsupported width");
+      return SMM_ERR_INVALID;
+  }
+  SMM_LAUNCH_CHECK("fwht2p_kernel");
+  return SMM_OK;
+}
+
+}  // namespace smm

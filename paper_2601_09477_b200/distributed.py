@@ -34,28 +34,30 @@ def row_bounds(n_rows: int, world: int, rank: int) -> tuple[int, int]:
     return shard_bounds(n_rows, world, rank)
 
 
-def compress_sharded(at_slab, b_slab, params: SketchParams, n_rows: int | None = None, n_cols: int | None = None,
-                     group=None, threads: int | None = None, all_reduce=None) -> ProductSketch:
+def compress_sharded(a_slab, b_slab, params: SketchParams, n_rows: int | None = None, n_cols: int | None = None,
+                     group=None, threads: int | None = None, all_reduce=None, a_layout: int = 0) -> ProductSketch:
     """Sketch of A @ B from this rank's k-slab; returns the full sketch on every rank.
 
-    at_slab: (k_local, n1) rows of A^T owned by this rank; b_slab: (k_local, n2).
+    a_slab: this rank's slab of A — rows of A^T (``a_layout=0``, k-major, shape
+    (k_local, n1)) or a column view A[:, k0:k1] (``a_layout=1``, k-minor, shape
+    (n1, k_local), used without a copy); b_slab: B[k0:k1] (k_local, n2).
     ``all_reduce`` (default: torch.distributed.all_reduce with SUM) is the one
     collective of the path.
     """
     from . import _device
 
     effective_threads(threads)
-    if at_slab.shape[0] != b_slab.shape[0]:
-        raise InvalidParameterError(f"inner slabs must match, got {at_slab.shape[0]} and {b_slab.shape[0]}")
-    dev = at_slab.device
+    kl = a_slab.shape[1] if a_layout == _device.KMINOR else a_slab.shape[0]
+    n1 = a_slab.shape[0] if a_layout == _device.KMINOR else a_slab.shape[1]
+    if kl != b_slab.shape[0]:
+        raise InvalidParameterError(f"inner slabs must match, got {kl} and {b_slab.shape[0]}")
     hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
-    kl = at_slab.shape[0]
-    acc = _device.compress_accumulate(at_slab, b_slab, hashes.packed_words(), params.d, params.log2b,
-                                      params.transform, 0, kl)
+    acc = _device.compress_accumulate(a_slab, b_slab, hashes.packed_words(), params.d, params.log2b,
+                                      params.transform, 0, kl, a_layout=a_layout)
     reduce_accumulator(acc, group=group, all_reduce=all_reduce)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)
     return ProductSketch(polys=polys, hashes=hashes, params=params,
-                         n_rows=n_rows if n_rows is not None else at_slab.shape[1],
+                         n_rows=n_rows if n_rows is not None else n1,
                          n_cols=n_cols if n_cols is not None else b_slab.shape[1])
 
 

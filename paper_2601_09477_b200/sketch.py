@@ -197,19 +197,26 @@ def _check_2d(m, what: str):
     return shp
 
 
-def _run(at, bm, params: SketchParams, threads, k0: int = 0, k1: int | None = None) -> ProductSketch:
-    """Steps 1-4 on device-resident operands (the reference's _run_kernel, sketch.py:238-260)."""
+def _run(a, b, params: SketchParams, threads, a_layout: int, b_layout: int = 0) -> ProductSketch:
+    """Steps 1-4 on device-resident operands (the reference's _run_kernel, sketch.py:238-260).
+
+    ``a`` is A (k-minor, the reference's ``a``) or A^T (k-major, its ``at``); ``b``
+    is B (k-major).  The library picks the kernel and transposes only what that
+    kernel needs (the reference always copies A.T, sketch.py:305-307).
+    """
     from . import _device
 
-    if at.shape[0] != bm.shape[0]:
-        raise InvalidParameterError(f"inner dimensions must match, got {at.shape[0]} and {bm.shape[0]}")
+    m_a = a.shape[1] if a_layout == _device.KMINOR else a.shape[0]
+    if m_a != b.shape[0]:
+        raise InvalidParameterError(f"inner dimensions must match, got {m_a} and {b.shape[0]}")
     effective_threads(threads)
     hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
     _check_depth(params)
-    k1 = at.shape[0] if k1 is None else k1
-    acc = _device.compress_accumulate(at, bm, hashes.packed_words(), params.d, params.log2b, params.transform, k0, k1)
+    acc = _device.compress_accumulate(a, b, hashes.packed_words(), params.d, params.log2b, params.transform, 0, m_a,
+                                      a_layout=a_layout, b_layout=b_layout)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)
-    return ProductSketch(polys=polys, hashes=hashes, params=params, n_rows=at.shape[1], n_cols=bm.shape[1])
+    n_rows = a.shape[0] if a_layout == _device.KMINOR else a.shape[1]
+    return ProductSketch(polys=polys, hashes=hashes, params=params, n_rows=n_rows, n_cols=b.shape[1])
 
 
 def _check_depth(params: SketchParams) -> None:
@@ -230,11 +237,8 @@ def compress(a, b, params: SketchParams, threads: int | None = None, device=None
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    av = _as_matrix(a, "left operand", dev)
-    bv = _as_matrix(b, "right operand", dev)
-    at = _device.transpose(av)  # the reference's ascontiguousarray(A.T) (sketch.py:305-307), on device
-    del av
-    return _run(at, bv, params, threads)
+    return _run(_as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev), params, threads,
+                _device.KMINOR)
 
 
 def compress_pretransposed(at, b, params: SketchParams, threads: int | None = None, device=None) -> ProductSketch:
@@ -248,7 +252,8 @@ def compress_pretransposed(at, b, params: SketchParams, threads: int | None = No
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    return _run(_as_matrix(at, "left operand (transposed)", dev), _as_matrix(b, "right operand", dev), params, threads)
+    return _run(_as_matrix(at, "left operand (transposed)", dev), _as_matrix(b, "right operand", dev), params,
+                threads, _device.KMAJOR)
 
 
 def compress_rect(a, b, params: SketchParams, threads: int | None = None, device=None) -> ProductSketch:
@@ -261,10 +266,8 @@ def compress_rect(a, b, params: SketchParams, threads: int | None = None, device
         raise InvalidParameterError(f"inner dimension must equal params.n={params.n}, got {sa} x {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    av = _as_matrix(a, "left operand", dev)
-    at = _device.transpose(av)
-    del av
-    return _run(at, _as_matrix(b, "right operand", dev), params, threads)
+    return _run(_as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev), params, threads,
+                _device.KMINOR)
 
 
 # ----------------------------------------------------------------------------- decompress
