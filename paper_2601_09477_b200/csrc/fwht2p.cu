@@ -87,7 +87,8 @@ __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const in
     const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b);
     const uint32_t sb = eval_signbit(h.f[2 + op][t], (uint64_t)i);
     const int32_t pos = off[row * (b + 1) + m] + atomicAdd(&fill[row * b + m], 1);
-    ent[row * nmax + pos] = (uint32_t)i | (sb << 31);
+    // entry: i (26 bits) | bucket & 31 (5 bits) | sign (1 bit)
+    ent[row * nmax + pos] = (uint32_t)i | ((m & 31u) << 26) | (sb << 31);
   }
 }
 
@@ -101,7 +102,7 @@ __global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax,
     for (int32_t a = e0 + 1; a < e1; ++a) {
       const uint32_t key = e[a];
       int32_t q = a - 1;
-      while (q >= e0 && (e[q] & 0x7fffffffu) > (key & 0x7fffffffu)) {
+      while (q >= e0 && (e[q] & 0x03ffffffu) > (key & 0x03ffffffu)) {
         e[q + 1] = e[q];
         --q;
       }
@@ -219,9 +220,9 @@ __device__ __forceinline__ void reg_fwht32(double (&v)[32], int qlo, int qhi) {
 
 // Pass 1: pull the 512 buckets [blk*512, blk*512+512) of operand op for the
 // 32 inner indices of k-tile kappa, FWHT over the 9 low bucket bits, write Y.
-__device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, int blk, double *S) {
+__device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int t, int slot, int op, int blk,
+                                           double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kappa = u / p.d, t = u % p.d;
   const bool kvalid = (int64_t)kappa * KT + lane < p.K;
   const double *X = p.X[op] + (p.k0 + (int64_t)kappa * KT + lane);
   const int64_t ld = p.ld[op];
@@ -229,7 +230,6 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, 
   const int64_t row = (int64_t)t * 2 + op;
   const int32_t *off = p.off + row * (p.bsz + 1);
   const uint32_t *ent = p.ent + row * p.nmax;
-  const HashFn hf = p.h.f[op][t];
   const int e_lo = off[base];
   const int e_hi = off[base + 32];
   double v[32];
@@ -243,12 +243,11 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, 
     for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
 #pragma unroll
     for (int s = 0; s < 8; ++s)
-      x[s] = (eb + s < e_hi && kvalid) ? __ldg(X + (int64_t)(es[s] & 0x7fffffffu) * ld) : 0.0;
+      x[s] = (eb + s < e_hi && kvalid) ? __ldg(X + (int64_t)(es[s] & 0x03ffffffu) * ld) : 0.0;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       if (eb + s < e_hi) {  // warp-uniform
-        const uint32_t i = es[s] & 0x7fffffffu;
-        const int j = (int)((int64_t)eval_bucket(hf, (uint64_t)i, p.B) - base);
+        const int j = (int)((es[s] >> 26) & 31u);
         const double val = (es[s] >> 31) ? -x[s] : x[s];
         switch (j) {
           SMM_CASE(0) SMM_CASE(1) SMM_CASE(2) SMM_CASE(3) SMM_CASE(4) SMM_CASE(5) SMM_CASE(6) SMM_CASE(7)
@@ -268,7 +267,7 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, 
 #pragma unroll
   for (int r = 0; r < 32; ++r) v[r] = S[((r & 15) * 32 + (warp + 16 * (r >> 4))) * 32 + lane];
   reg_fwht32(v, 0, 4);  // bucket bits 5-8
-  double *Yd = p.Y + (((int64_t)(u % p.nslot) * 2 + op) * p.bsz + (int64_t)blk * 512) * KT + lane;
+  double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 512) * KT + lane;
   const uint64_t pol = policy_evict_last();
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
@@ -277,11 +276,11 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int u, int op, 
   }
 }
 
-__device__ __forceinline__ void p1_item(const TwoPassArgs &p, int u, int blk, double *S) {
+__device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, int slot, int blk, double *S) {
 #pragma unroll 1
   for (int op = 0; op < 2; ++op) {
     if (op == 1) __syncthreads();  // every warp has read operand 0's exchange data from S
-    p1_operand(p, u, op, blk, S);
+    p1_operand(p, kappa, t, slot, op, blk, S);
   }
 }
 
@@ -289,12 +288,13 @@ __device__ __forceinline__ void p1_item(const TwoPassArgs &p, int u, int blk, do
 // finish the transform of both operands over the hb high bits, multiply, sum
 // over the 32 inner indices and extend the accumulator.
 template <int HB>
-__device__ __forceinline__ void p2_item(const TwoPassArgs &p, int u, int s, uint32_t tmem, const int *acc_flag) {
+__device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, int slot, int s, uint32_t tmem,
+                                        const int *acc_flag, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the accumulator of (t, s) must already hold k-tiles < kappa: poll early, check before the update
   int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
   const int wq = warp & 3, wh = warp >> 2;
-  const int kappa = u / p.d, t = u % p.d;
+  
   constexpr int hb = HB;
   const int hmask = (1 << hb) - 1;
   const int64_t lo0 = (int64_t)s << (P1_BITS - hb);
@@ -309,7 +309,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int u, int s, uint
   double v[32];
   const uint64_t pol = policy_evict_first();
   for (int op = 0; op < 2; ++op) {
-    const double *Ys = p.Y + ((int64_t)(u % p.nslot) * 2 + op) * p.bsz * KT + lane;
+    const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + lane;
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       const int sg = r | (wh << 5) | (wq << 7);
@@ -319,13 +319,12 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int u, int s, uint
     reg_fwht32(v, 0, hb < 5 ? hb : 5);
     // last use of these Y rows: drop the L2 lines without write-back
     __syncwarp();
-    if ((lane & 15) == 0) {
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int sg = r | (wh << 5) | (wq << 7);
-        const int64_t bucket = (int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb);
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(Ys + bucket * KT) : "memory");
-      }
+    {
+      // lane l drops both 128-byte lines of the row it read as register l
+      const int sg = lane | (wh << 5) | (wq << 7);
+      const double *row = Ys - lane + ((int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb)) * KT;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(row) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + 16) : "memory");
     }
     if (hb > 5) {
       // TMEM exchange: register bits 3,4 <-> warp bits wh (slice bits 5,6), among quadrant-mates
@@ -356,17 +355,16 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int u, int s, uint
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
   }
-  // sum over the 32 inner indices (lanes): transpose-reduce, lane l ends with register l
+  // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory
+  // (idle during pass 2): lane l ends with register l summed over all lanes, in lane order
+  double *W = S + warp * 1024;
 #pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    const bool upper = (lane & m) != 0;
+  for (int r = 0; r < 32; ++r) W[r * 32 + (lane ^ r)] = v[r];
+  __syncwarp();
+  double sum = 0.0;
 #pragma unroll
-    for (int r = 0; r < m; ++r) {
-      const double send = upper ? v[r] : v[r + m];
-      const double keep = upper ? v[r + m] : v[r];
-      v[r] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-    }
-  }
+  for (int j = 0; j < 32; ++j) sum += W[lane * 32 + (j ^ lane)];
+  v[0] = sum;
   if (kappa == 0) {
     __stcg(a, v[0]);
   } else if (acc_ready) {
@@ -416,7 +414,7 @@ template <int HB>
 __global__ void __launch_bounds__(P_THREADS, 1) fwht2p_kernel(TwoPassArgs p) {
   extern __shared__ __align__(16) double S[];  // 16 warps x 32 x 32 doubles = 128 KB
   __shared__ uint32_t s_tmem;
-  __shared__ int s_item[4];
+  __shared__ int s_item[7];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (warp == 0) {
@@ -456,24 +454,28 @@ __global__ void __launch_bounds__(P_THREADS, 1) fwht2p_kernel(TwoPassArgs p) {
       s_item[1] = it.is_p1;
       s_item[2] = it.u;
       s_item[3] = it.idx;
+      s_item[4] = it.u / p.d;
+      s_item[5] = it.u % p.d;
+      s_item[6] = it.u % p.nslot;
     }
     __syncthreads();  // [A]
     if (!s_item[0]) break;
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
+    const int kappa = s_item[4], t = s_item[5], slot = s_item[6];
     if (tid == 0) {
       // prefetch the ticket after next now; its round trip overlaps this item's work
       cur = nxt;
       nxt = (nxt < total) ? (int64_t)atomicAdd(ticket, 1) : nxt;
     }
-    if (is_p1) p1_item(p, u, idx, S);
-    else p2_item<HB>(p, u, idx, tmem, acc_cnt + (u % p.d) * p.nblk + idx);
+    if (is_p1) p1_item(p, kappa, t, slot, idx, S);
+    else p2_item<HB>(p, kappa, t, slot, idx, tmem, acc_cnt + t * p.nblk + idx, S);
     tc_fence_before();
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
     tc_fence_after();
     if (tid == 0) {
       if (is_p1) red_release_add(done1 + u, 1);
       else {
-        red_release_add(acc_cnt + (u % p.d) * p.nblk + idx, 1);
+        red_release_add(acc_cnt + t * p.nblk + idx, 1);
         red_release_add(done2 + u, 1);
       }
     }
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) fwht2p_kernel(TwoPassArgs p) {
 static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
-  return log2b >= P1_BITS && log2b <= P1_BITS + 7 && n1 < ((int64_t)1 << 31) && n2 < ((int64_t)1 << 31);
+  return log2b >= P1_BITS && log2b <= P1_BITS + 7 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
 static int nslots_for(int log2b) {
