@@ -24,13 +24,30 @@
 // extends the accumulator after P2(kappa-1, t, s)) are dispensed earlier, so
 // spinning on them cannot deadlock; accumulator updates happen in k order, so
 // results are bit-reproducible.
+#include <cstdlib>
+
 #include "plan.cuh"
 
 namespace smm {
 
-constexpr int P_THREADS = 512;
+constexpr int P_THREADS = 256;
 constexpr int KT = 32;
-constexpr int P1_BITS = 9;
+constexpr int P1_BITS = 8;
+#define SMM_LAG 1  // P2(u) is dispensed LAG groups after P1(u) (2 was measured slower on cfg3)
+
+// Optional phase profiler (env SMM_PROFILE=1): thread 0 of every CTA accumulates
+// clock64 deltas between marks; printed by the host after the launch.
+__shared__ long long s_prof[16];
+__shared__ long long s_prof_last;
+__device__ int g_prof_on;
+#define PROF_MARK(k)                                 \
+  do {                                               \
+    if (g_prof_on && threadIdx.x == 0) {             \
+      const long long _n = clock64();                \
+      s_prof[k] += _n - s_prof_last;                 \
+      s_prof_last = _n;                              \
+    }                                                \
+  } while (0)
 
 // ------------------------------------------------------------------ CSR plan
 // entries sorted by (bucket, i) per (t, op): off [d][2][b+1], ent [d][2][nmax] = i | sign << 31
@@ -42,7 +59,7 @@ __global__ void csr_count_kernel(SketchHashes h, int64_t n1, int64_t n2, int32_t
     const int64_t q = x % per;
     const int op = q < n1 ? 0 : 1;
     const int64_t i = op ? q - n1 : q;
-    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b);
+    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b) & (uint32_t)(b - 1);  // bucket within slice
     atomicAdd(&cnt[((int64_t)t * 2 + op) * b + m], 1);
   }
 }
@@ -84,7 +101,7 @@ __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const in
     const int op = q < n1 ? 0 : 1;
     const int64_t i = op ? q - n1 : q;
     const int64_t row = (int64_t)t * 2 + op;
-    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b);
+    const uint32_t m = eval_bucket(h.f[op][t], (uint64_t)i, h.log2b) & (uint32_t)(b - 1);  // bucket within slice
     const uint32_t sb = eval_signbit(h.f[2 + op][t], (uint64_t)i);
     const int32_t pos = off[row * (b + 1) + m] + atomicAdd(&fill[row * b + m], 1);
     // entry: i (26 bits) | bucket & 31 (5 bits) | sign (1 bit)
@@ -118,12 +135,14 @@ struct TwoPassArgs {
   int64_t ld[2];
   int64_t k0, K;
   int B, hb, d, nblk, ntiles, U, nslot;
+  int F, LB, df;  // top-level fold: F = b / 2^LB slices of 2^LB buckets; df = d * F
   const int32_t *off;
   const uint32_t *ent;
   int64_t nmax, bsz;
   double *Y;   // [nslot][2][b][KT]
   double *acc; // [d][b]
   int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
+  long long *prof;  // [16] phase cycles (nullable)
 };
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -218,25 +237,43 @@ __device__ __forceinline__ void reg_fwht32(double (&v)[32], int qlo, int qhi) {
     v[J] += val;    \
     break;
 
-// Pass 1: pull the 512 buckets [blk*512, blk*512+512) of operand op for the
-// 32 inner indices of k-tile kappa, FWHT over the 9 low bucket bits, write Y.
-__device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int t, int slot, int op, int blk,
-                                           double *S) {
+// Pass 1: pull the 256 buckets [blk*256, blk*256+256) of operand op for the
+// 32 inner indices of k-tile kappa, FWHT over the 8 low bucket bits, write Y.
+// Warp w owns buckets blk*256 + w*32 + j (j = register index), lanes = k.
+// CSR range of one warp's 32 buckets and its first 8 entries, fetched ahead of use
+struct PullHead {
+  int e_lo, e_hi;
+  uint32_t first;
+};
+
+__device__ __forceinline__ PullHead pull_head(const TwoPassArgs &p, int t, int op, int blk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blk * 256 + warp * 32;
+  const int64_t row = (int64_t)t * 2 + op;
+  const int32_t *off = p.off + row * (p.bsz + 1);
+  PullHead h;
+  h.e_lo = __ldg(off + base);
+  h.e_hi = __ldg(off + base + 32);
+  h.first = (lane < 8 && h.e_lo + lane < h.e_hi) ? __ldg(p.ent + row * p.nmax + h.e_lo + lane) : 0u;
+  return h;
+}
+
+__device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
+                                           double *S, const PullHead &hd) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool kvalid = (int64_t)kappa * KT + lane < p.K;
   const double *X = p.X[op] + (p.k0 + (int64_t)kappa * KT + lane);
   const int64_t ld = p.ld[op];
-  const int64_t base = (int64_t)blk * 512 + warp * 32;
   const int64_t row = (int64_t)t * 2 + op;
-  const int32_t *off = p.off + row * (p.bsz + 1);
   const uint32_t *ent = p.ent + row * p.nmax;
-  const int e_lo = off[base];
-  const int e_hi = off[base + 32];
+  const int e_lo = hd.e_lo;
+  const int e_hi = hd.e_hi;
   double v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = 0.0;
   for (int eb = e_lo; eb < e_hi; eb += 8) {
-    const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
+    const uint32_t mine =
+        eb == e_lo ? hd.first : ((lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u);
     uint32_t es[8];
     double x[8];
 #pragma unroll
@@ -248,7 +285,10 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
     for (int s = 0; s < 8; ++s) {
       if (eb + s < e_hi) {  // warp-uniform
         const int j = (int)((es[s] >> 26) & 31u);
-        const double val = (es[s] >> 31) ? -x[s] : x[s];
+        uint32_t neg = es[s] >> 31;
+        if (p.F > 1)  // fold character of slice a: (-1)^popcount(a & (h(i) >> LB))
+          neg ^= __popc((eval_bucket(p.h.f[op][t], (uint64_t)(es[s] & 0x03ffffffu), p.B) >> p.LB) & (uint32_t)a) & 1u;
+        const double val = neg ? -x[s] : x[s];
         switch (j) {
           SMM_CASE(0) SMM_CASE(1) SMM_CASE(2) SMM_CASE(3) SMM_CASE(4) SMM_CASE(5) SMM_CASE(6) SMM_CASE(7)
           SMM_CASE(8) SMM_CASE(9) SMM_CASE(10) SMM_CASE(11) SMM_CASE(12) SMM_CASE(13) SMM_CASE(14) SMM_CASE(15)
@@ -259,87 +299,88 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
       }
     }
   }
+  PROF_MARK(3);
   reg_fwht32(v, 0, 5);  // bucket bits 0-4
-  // exchange: warp bits (bucket bits 5-8) <-> register bits 0-3
+  // exchange: warp bits (bucket bits 5-7) <-> register bits 0-2
 #pragma unroll
   for (int j = 0; j < 32; ++j) S[(warp * 32 + j) * 32 + lane] = v[j];
+  PROF_MARK(4);
   __syncthreads();
+  PROF_MARK(5);
 #pragma unroll
-  for (int r = 0; r < 32; ++r) v[r] = S[((r & 15) * 32 + (warp + 16 * (r >> 4))) * 32 + lane];
-  reg_fwht32(v, 0, 4);  // bucket bits 5-8
-  double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 512) * KT + lane;
+  for (int r = 0; r < 32; ++r) v[r] = S[((r & 7) * 32 + (warp + 8 * (r >> 3))) * 32 + lane];
+  reg_fwht32(v, 0, 3);  // bucket bits 5-7
+  PROF_MARK(6);
+  double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 256) * KT + lane;
   const uint64_t pol = policy_evict_last();
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
-    const int bl = (warp + 16 * (r >> 4)) + 32 * (r & 15);
+    const int bl = (warp + 8 * (r >> 3)) + 32 * (r & 7);
     st_hint(Yd + (int64_t)bl * KT, v[r], pol);
   }
+  PROF_MARK(7);
 }
 
-__device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, int slot, int blk, double *S) {
-#pragma unroll 1
-  for (int op = 0; op < 2; ++op) {
-    if (op == 1) __syncthreads();  // every warp has read operand 0's exchange data from S
-    p1_operand(p, kappa, t, slot, op, blk, S);
-  }
+__device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double *S,
+                                        const PullHead &hd0) {
+  const PullHead hd1 = pull_head(p, t, 1, blk);  // operand 1's head lands while operand 0 computes
+  p1_operand(p, kappa, t, a, slot, 0, blk, S, hd0);
+  __syncthreads();  // every warp has read operand 0's exchange data from S
+  p1_operand(p, kappa, t, a, slot, 1, blk, S, hd1);
 }
 
-// Pass 2: for slice s (512 buckets: every high-bit value x 2^(9-hb) low values)
+// Pass 2: for slice s (256 buckets: every high-bit value x 2^(8-hb) low values)
 // finish the transform of both operands over the hb high bits, multiply, sum
-// over the 32 inner indices and extend the accumulator.
+// over the 32 inner indices and extend the accumulator.  Slice bit sigma:
+// registers <- sigma 0-4, warp <- sigma 5-7; bucket = hi * 256 + lo.
 template <int HB>
-__device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, int slot, int s, uint32_t tmem,
+__device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s, uint32_t tmem,
                                         const int *acc_flag, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the accumulator of (t, s) must already hold k-tiles < kappa: poll early, check before the update
   int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
   const int wq = warp & 3, wh = warp >> 2;
-  
   constexpr int hb = HB;
   const int hmask = (1 << hb) - 1;
   const int64_t lo0 = (int64_t)s << (P1_BITS - hb);
   // this lane's accumulator bucket after the lane reduction (fixed by the mapping)
-  const int sg_acc = hb > 5 ? ((lane & 7) | (wh << 3) | ((lane >> 3) << 5) | (wq << 7)) : (lane | (wh << 5) | (wq << 7));
-  double *a = p.acc + (int64_t)t * p.bsz + (int64_t)(sg_acc & hmask) * 512 + lo0 + (sg_acc >> hb);
+  const int sg_acc = hb > 5 ? ((lane & 3) | (warp << 2) | ((lane >> 2) << 5)) : (lane | (warp << 5));
+  double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)(sg_acc & hmask) * 256 + lo0 + (sg_acc >> hb);
   // usually the previous k-tile's update of this slice finished long ago: fetch the old value early
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = (kappa > 0 && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * wq) << 16);
-  const uint32_t col_fa = (uint32_t)(wh * 64), col_x = (uint32_t)(256 + wh * 64);
+  const uint32_t col_fa = (uint32_t)(wh * 64);
   double v[32];
   const uint64_t pol = policy_evict_first();
+#pragma unroll 1
   for (int op = 0; op < 2; ++op) {
     const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + lane;
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int sg = r | (wh << 5) | (wq << 7);
-      const int64_t bucket = (int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb);
+      const int sg = r | (warp << 5);
+      const int64_t bucket = (int64_t)(sg & hmask) * 256 + lo0 + (sg >> hb);
       v[r] = ld_hint(Ys + bucket * KT, pol);
     }
+    PROF_MARK(8);
     reg_fwht32(v, 0, hb < 5 ? hb : 5);
     // last use of these Y rows: drop the L2 lines without write-back
     __syncwarp();
     {
-      // lane l drops both 128-byte lines of the row it read as register l
-      const int sg = lane | (wh << 5) | (wq << 7);
-      const double *row = Ys - lane + ((int64_t)(sg & hmask) * 512 + lo0 + (sg >> hb)) * KT;
+      const int sg = lane | (warp << 5);
+      const double *row = Ys - lane + ((int64_t)(sg & hmask) * 256 + lo0 + (sg >> hb)) * KT;
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(row) : "memory");
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + 16) : "memory");
     }
     if (hb > 5) {
-      // TMEM exchange: register bits 3,4 <-> warp bits wh (slice bits 5,6), among quadrant-mates
+      // shared-memory exchange: warp bits (sigma 5-7) <-> register bits 2-4
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_st8(tq + col_x + 16 * c, v + 8 * c);
-      tmem_wait_st();
-      tc_fence_before();
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + wq) : "memory");  // the 4 quadrant-mate warps
-      tc_fence_after();
+      for (int r = 0; r < 32; ++r) S[(warp * 32 + r) * 32 + lane] = v[r];
+      __syncthreads();
 #pragma unroll
-      for (int src = 0; src < 4; ++src) tmem_ld8(tq + (uint32_t)(256 + src * 64 + 16 * wh), v + 8 * src);
-      reg_fwht32(v, 3, 3 + (hb - 5));
-      tc_fence_before();
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + wq) : "memory");  // exchange area is reused by the next operand
-      tc_fence_after();
+      for (int r = 0; r < 32; ++r) v[r] = S[((r >> 2) * 32 + ((r & 3) | (warp << 2))) * 32 + lane];
+      reg_fwht32(v, 2, 2 + (hb - 5));
+      __syncthreads();  // S is reused by the next exchange / the reduction
     }
     if (op == 0) {
 #pragma unroll
@@ -347,6 +388,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
       tmem_wait_st();
     }
   }
+  PROF_MARK(9);
   // product FA * FB (FB in v)
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -355,8 +397,8 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
   }
-  // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory
-  // (idle during pass 2): lane l ends with register l summed over all lanes, in lane order
+  // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory:
+  // lane l ends with register l summed over all lanes, in lane order
   double *W = S + warp * 1024;
 #pragma unroll
   for (int r = 0; r < 32; ++r) W[r * 32 + (lane ^ r)] = v[r];
@@ -364,11 +406,10 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   double sum = 0.0;
 #pragma unroll
   for (int j = 0; j < 32; ++j) sum += W[lane * 32 + (j ^ lane)];
-  v[0] = sum;
   if (kappa == 0) {
-    __stcg(a, v[0]);
+    __stcg(a, sum);
   } else if (acc_ready) {
-    __stcg(a, acc_old + v[0]);
+    __stcg(a, acc_old + sum);
   } else {
     if (lane == 0)
       while (flag < kappa) {
@@ -376,7 +417,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
         flag = ld_relaxed(acc_flag);
       }
     __syncwarp();
-    __stcg(a, __ldcg(a) + v[0]);
+    __stcg(a, __ldcg(a) + sum);
   }
 }
 
@@ -385,131 +426,190 @@ struct Item {
   int is_p1, u, idx;
 };
 
-__device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos) {
-  const int G1 = p.nblk, G2 = p.nblk;
+__device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, int log2g) {
+  // prologue: P1 of units 0..LAG-1; then groups g = 0..U-1: [P1(g+LAG) x nblk][P2(g) x nblk]
+  // (the P1 part is absent once g+LAG >= U).  2*nblk is a power of two.
+  const int G1 = p.nblk;
+  const int pro_units = p.U < SMM_LAG ? p.U : SMM_LAG;
   Item it;
   it.pos = pos;
-  if (pos < G1) {
-    it.is_p1 = 1; it.u = 0; it.idx = (int)pos;
+  if (pos < (int64_t)pro_units * G1) {
+    it.is_p1 = 1; it.u = (int)(pos / G1); it.idx = (int)(pos % G1);
     return it;
   }
-  const int q = (int)(pos - G1);
-  const int regular = (p.U - 1) * (G1 + G2);
+  const int q = (int)(pos - (int64_t)pro_units * G1);
+  const int full = p.U > SMM_LAG ? p.U - SMM_LAG : 0;
+  const int regular = full << log2g;
   if (q < regular) {
-    const unsigned g = (unsigned)q / (unsigned)(G1 + G2);
-    const int r = q - (int)g * (G1 + G2);
-    if (r < G1) { it.is_p1 = 1; it.u = g + 1; it.idx = r; }
+    const int g = q >> log2g;
+    const int r = q & ((1 << log2g) - 1);
+    if (r < G1) { it.is_p1 = 1; it.u = g + SMM_LAG; it.idx = r; }
     else { it.is_p1 = 0; it.u = g; it.idx = r - G1; }
   } else {
-    it.is_p1 = 0; it.u = p.U - 1; it.idx = (int)(q - regular);
+    const int q2 = q - regular;
+    it.is_p1 = 0; it.u = full + q2 / G1; it.idx = q2 % G1;
   }
   return it;
 }
 
-__device__ __forceinline__ void red_release_add(int *ptr, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+__device__ __forceinline__ void red_add(int *ptr, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
 }
 
 template <int HB>
-__global__ void __launch_bounds__(P_THREADS, 1) fwht2p_kernel(TwoPassArgs p) {
-  extern __shared__ __align__(16) double S[];  // 16 warps x 32 x 32 doubles = 128 KB
+__global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
+  extern __shared__ __align__(16) double S[];  // 8 warps x 32 x 32 doubles = 64 KB
   __shared__ uint32_t s_tmem;
-  __shared__ int s_item[7];
+  __shared__ int s_item[12];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (tid < 16) s_prof[tid] = 0;
+  if (tid == 0) s_prof_last = clock64();
   int *ticket = p.ctr;
   int *done1 = p.ctr + 1;
   int *done2 = done1 + p.U;
   int *acc_cnt = done2 + p.U;
   const int G1 = p.nblk, G2 = p.nblk;  // P1 items: one block, both operands; P2 items: one slice
+  const int log2g = 31 - __clz(2 * p.nblk);
   const int64_t total = (int64_t)p.U * (G1 + G2);
-  // thread 0 owns the scheduling state: the current ticket and one prefetched ticket
-  int64_t cur = 0, nxt = 0;
-  int ver1 = -1, ver2 = -1;  // units whose P1 / P2 items are all known complete (prefix)
+  // Thread 0 runs the scheduler one item ahead: the ticket after next and the
+  // dependency counter of the next item are fetched while the current item
+  // computes.  Thread 32 publishes an item's completion (fence + relaxed adds)
+  // right after the item's closing barrier, concurrently with thread 0's
+  // scheduling, so the fence latency is not serialised with it.  Every warp
+  // prefetches the CSR head of the next pass-1 item during the current item.
+  int64_t nxt = 0;
+  Item itn;
+  const int *dep_ptr = nullptr;
+  int dep_target = 0, dep_val = 0;
+  int ver1 = -1, ver2 = -1;  // highest unit whose P1 / P2 completion this CTA has seen
+  auto probe = [&](const Item &it) {
+    dep_ptr = nullptr;
+    if (it.pos >= total) return;
+    if (it.is_p1) {
+      const int need = it.u - p.nslot;
+      if (need > ver2) { dep_ptr = done2 + need; dep_target = G2; }
+    } else {
+      if (it.u > ver1) { dep_ptr = done1 + it.u; dep_target = G1; }
+    }
+    if (dep_ptr) dep_val = ld_relaxed(dep_ptr);
+  };
   if (tid == 0) {
-    cur = atomicAdd(ticket, 1);
+    const int64_t cur = atomicAdd(ticket, 1);
     nxt = atomicAdd(ticket, 1);
+    itn = decode_item(p, cur, log2g);
+    probe(itn);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  PullHead hd_next;
+  bool hd_valid = false;
   while (true) {
     if (tid == 0) {
-      Item it = decode_item(p, cur);
-      if (cur < total) {
-        // dependencies (dispensed earlier, so this cannot deadlock); acquire orders the reads below
-        if (it.is_p1) {
-          for (; ver2 < it.u - p.nslot; ++ver2) wait_geq(done2 + ver2 + 1, G2);
-        } else {
-          for (; ver1 < it.u; ++ver1) wait_geq(done1 + ver1 + 1, G1);
+      const Item it = itn;
+      if (dep_ptr) {  // dependency of this item (dispensed earlier: cannot deadlock)
+        while (dep_val < dep_target) {
+          __nanosleep(64);
+          dep_val = ld_relaxed(dep_ptr);
         }
+        if (it.is_p1) ver2 = it.u - p.nslot;
+        else ver1 = it.u;
       }
-      s_item[0] = cur < total ? 1 : 0;
+      __threadfence();  // acquire side of the counters observed above
+      const Item in = decode_item(p, nxt, log2g);
+      s_item[0] = it.pos < total ? 1 : 0;
       s_item[1] = it.is_p1;
       s_item[2] = it.u;
       s_item[3] = it.idx;
-      s_item[4] = it.u / p.d;
-      s_item[5] = it.u % p.d;
+      s_item[4] = it.u / p.df;
+      s_item[5] = (it.u % p.df) / p.F;
       s_item[6] = it.u % p.nslot;
+      s_item[10] = (it.u % p.df) % p.F;
+      s_item[7] = (in.pos < total && in.is_p1) ? 1 : 0;
+      s_item[8] = (in.u % p.df) / p.F;
+      s_item[9] = in.idx;
+      itn = in;
     }
-    __syncthreads();  // [A]
-    if (!s_item[0]) break;
-    const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
-    const int kappa = s_item[4], t = s_item[5], slot = s_item[6];
-    if (tid == 0) {
-      // prefetch the ticket after next now; its round trip overlaps this item's work
-      cur = nxt;
-      nxt = (nxt < total) ? (int64_t)atomicAdd(ticket, 1) : nxt;
-    }
-    if (is_p1) p1_item(p, kappa, t, slot, idx, S);
-    else p2_item<HB>(p, kappa, t, slot, idx, tmem, acc_cnt + t * p.nblk + idx, S);
     tc_fence_before();
-    __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
+    PROF_MARK(0);
+    __syncthreads();  // [A]
+    PROF_MARK(1);
     tc_fence_after();
-    if (tid == 0) {
-      if (is_p1) red_release_add(done1 + u, 1);
+    const int go = s_item[0];
+    const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
+    const int kappa = s_item[4], t = s_item[5], slot = s_item[6], asl = s_item[10];
+    const int next_p1 = s_item[7], next_t = s_item[8], next_idx = s_item[9];
+    if (tid == 0 && go) {
+      probe(itn);
+      nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
+    }
+    if (!go) break;
+    PullHead hd_cur;
+    if (is_p1) hd_cur = hd_valid ? hd_next : pull_head(p, t, 0, idx);
+    hd_valid = next_p1 != 0;
+    if (hd_valid) hd_next = pull_head(p, next_t, 0, next_idx);  // lands while this item computes
+    if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur);
+    else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_cnt + (t * p.F + asl) * p.nblk + idx, S);
+    tc_fence_before();
+    PROF_MARK(2);
+    __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
+    PROF_MARK(10);
+    tc_fence_after();
+    if (tid == 32) {  // publish this item's completion
+      __threadfence();
+      if (is_p1) red_add(done1 + u, 1);
       else {
-        red_release_add(acc_cnt + t * p.nblk + idx, 1);
-        red_release_add(done2 + u, 1);
+        red_add(acc_cnt + (t * p.F + asl) * p.nblk + idx, 1);
+        red_add(done2 + u, 1);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (p.prof && tid == 0)
+    for (int k = 0; k < 16; ++k) atomicAdd((unsigned long long *)&p.prof[k], (unsigned long long)s_prof[k]);
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // ------------------------------------------------------------------ host
 static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
+constexpr int MAX_LB = 16;  // per-slice transform bits handled by the two passes (8 + 8)
+
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
-  return log2b >= P1_BITS && log2b <= P1_BITS + 7 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
+  return log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
-static int nslots_for(int log2b) {
-  const int64_t yunit = (int64_t)2 * ((int64_t)1 << log2b) * KT * 8;
-  return yunit * 3 <= ((int64_t)100 << 20) ? 3 : 3;
+static int nslots_for(int) { return 3; }
+
+// geometry: LB-bit slices, F = 2^(log2b - LB) of them (the fold of DESIGN.md §5)
+static void fwht2p_geometry(int log2b, int &LB, int &F) {
+  LB = log2b < MAX_LB ? log2b : MAX_LB;
+  F = 1 << (log2b - LB);
 }
 
 int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
-  const int64_t b = (int64_t)1 << log2b;
+  int LB, F;
+  fwht2p_geometry(log2b, LB, F);
+  const int64_t bs = (int64_t)1 << LB;
   const int64_t nmax = n1 > n2 ? n1 : n2;
   const int64_t ntiles = (K + KT - 1) / KT;
-  const int64_t U = ntiles * d;
-  const int64_t nblk = b >> P1_BITS;
+  const int64_t U = ntiles * d * F;
+  const int64_t nblk = bs >> P1_BITS;
   int64_t w = 0;
-  w += pad256((int64_t)d * 2 * (b + 1) * 4);  // off
-  w += pad256((int64_t)d * 2 * b * 4);        // cnt / fill
-  w += pad256((int64_t)d * 2 * nmax * 4);     // ent
-  w += pad256((int64_t)nslots_for(log2b) * 2 * b * KT * 8);  // Y ring
-  w += pad256((1 + 2 * U + (int64_t)d * nblk) * 4);          // counters
+  w += pad256((int64_t)d * 2 * (bs + 1) * 4);  // off
+  w += pad256((int64_t)d * 2 * bs * 4);        // cnt / fill
+  w += pad256((int64_t)d * 2 * nmax * 4);      // ent
+  w += pad256((int64_t)nslots_for(log2b) * 2 * bs * KT * 8);  // Y ring
+  w += pad256((1 + 2 * U + (int64_t)d * F * nblk) * 4);       // counters
   return w;
 }
 
@@ -517,7 +617,10 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
                       int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
                       cudaStream_t s) {
   const int d = h.d, log2b = h.log2b;
+  int LB, F;
+  fwht2p_geometry(log2b, LB, F);
   const int64_t b = (int64_t)1 << log2b;
+  const int64_t bs = (int64_t)1 << LB;
   const int64_t K = k1 - k0;
   const int64_t nmax = n1 > n2 ? n1 : n2;
   if (ws_bytes < fwht2p_workspace(d, log2b, n1, n2, K)) {
@@ -526,18 +629,18 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   }
   char *q = ws;
   int32_t *off = (int32_t *)q;
-  q += pad256((int64_t)d * 2 * (b + 1) * 4);
+  q += pad256((int64_t)d * 2 * (bs + 1) * 4);
   int32_t *cnt = (int32_t *)q;
-  q += pad256((int64_t)d * 2 * b * 4);
+  q += pad256((int64_t)d * 2 * bs * 4);
   uint32_t *ent = (uint32_t *)q;
   q += pad256((int64_t)d * 2 * nmax * 4);
   double *Y = (double *)q;
   const int nslot = nslots_for(log2b);
-  q += pad256((int64_t)nslot * 2 * b * KT * 8);
+  q += pad256((int64_t)nslot * 2 * bs * KT * 8);
   int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;
-  const int64_t U = ntiles * d;
-  const int nblk = (int)(b >> P1_BITS);
+  const int64_t U = ntiles * d * F;
+  const int nblk = (int)(bs >> P1_BITS);
   if (K <= 0) {
     SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
     return SMM_OK;
@@ -546,27 +649,27 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     set_error("inner range too large for one call");
     return SMM_ERR_INVALID;
   }
-  // plan (CSR by bucket)
-  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  // plan (CSR by bucket within the slice)
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * bs * 4, s), "csr memset");
   const int64_t nin = (int64_t)d * (n1 + n2);
   int64_t blocks = ceil_div(nin, 256);
   if (blocks > 8192) blocks = 8192;
   if (nin > 0) {
-    csr_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, b);
+    csr_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, bs);
     SMM_LAUNCH_CHECK("csr_count_kernel");
   }
-  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, b);
+  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, bs);
   SMM_LAUNCH_CHECK("csr_scan_kernel");
-  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * bs * 4, s), "csr memset");
   if (nin > 0) {
-    csr_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, b);
+    csr_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, bs);
     SMM_LAUNCH_CHECK("csr_fill_kernel");
-    int64_t sb = ceil_div((int64_t)d * 2 * b, 256);
+    int64_t sb = ceil_div((int64_t)d * 2 * bs, 256);
     if (sb > 8192) sb = 8192;
-    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, b, d * 2);
+    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, bs, d * 2);
     SMM_LAUNCH_CHECK("csr_sort_kernel");
   }
-  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * nblk) * 4, s), "counter memset");
+  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * F * nblk) * 4, s), "counter memset");
   TwoPassArgs p;
   p.h = h;
   p.X[0] = xa;
@@ -576,7 +679,10 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.k0 = k0;
   p.K = K;
   p.B = log2b;
-  p.hb = log2b - P1_BITS;
+  p.hb = LB - P1_BITS;
+  p.F = F;
+  p.LB = LB;
+  p.df = d * F;
   p.d = d;
   p.nblk = nblk;
   p.ntiles = (int)ntiles;
@@ -585,13 +691,22 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.off = off;
   p.ent = ent;
   p.nmax = nmax;
-  p.bsz = b;
+  p.bsz = bs;
   p.Y = Y;
   p.acc = acc;
   p.ctr = ctr;
-  const size_t smem = (size_t)16 * 32 * 32 * 8;
-  // one persistent CTA per SM (TMEM is fully allocated per CTA, so co-residency is exactly 1)
-  const int G = num_sms();
+  p.prof = nullptr;
+  static const bool prof_on = getenv("SMM_PROFILE") != nullptr;
+  if (prof_on) {
+    cudaMalloc((void **)&p.prof, 16 * sizeof(long long));
+    cudaMemset(p.prof, 0, 16 * sizeof(long long));
+    int one = 1;
+    cudaMemcpyToSymbol(g_prof_on, &one, sizeof(int));
+  }
+  const size_t smem = (size_t)8 * 32 * 32 * 8;
+  // two persistent CTAs per SM (256 threads, 128 registers, 64 KB smem, 128 TMEM columns each):
+  // one CTA's barriers and memory latency overlap the other's FP64 work
+  const int G = 2 * num_sms();
   switch (p.hb) {
 #define SMM_LAUNCH_HB(H)                                                                                 \
   case H:                                                                                                \
@@ -600,13 +715,24 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     fwht2p_kernel<H><<<G, P_THREADS, smem, s>>>(p);                                                      \
     break;
     SMM_LAUNCH_HB(0) SMM_LAUNCH_HB(1) SMM_LAUNCH_HB(2) SMM_LAUNCH_HB(3)
-    SMM_LAUNCH_HB(4) SMM_LAUNCH_HB(5) SMM_LAUNCH_HB(6) SMM_LAUNCH_HB(7)
+    SMM_LAUNCH_HB(4) SMM_LAUNCH_HB(5) SMM_LAUNCH_HB(6) SMM_LAUNCH_HB(7) SMM_LAUNCH_HB(8)
 #undef SMM_LAUNCH_HB
     default:
       set_error("two-pass kernel: unsupported width");
       return SMM_ERR_INVALID;
   }
   SMM_LAUNCH_CHECK("fwht2p_kernel");
+  if (p.prof) {
+    long long h[16];
+    cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost);
+    double tot = 0;
+    for (int k = 0; k < 16; ++k) tot += (double)h[k];
+    fprintf(stderr, "[fwht2p profile, %% of thread-0 cycles over all CTAs]");
+    for (int k = 0; k < 16; ++k)
+      if (h[k]) fprintf(stderr, " m%d=%.1f", k, 100.0 * (double)h[k] / tot);
+    fprintf(stderr, "\n");
+    cudaFree(p.prof);
+  }
   return SMM_OK;
 }
 
