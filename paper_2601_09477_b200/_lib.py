@@ -7,13 +7,15 @@ visible, every hot-path call raises — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import InvalidParameterError, SketchmmError
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_smm_b200.so"
+# SMM_LIB selects an experimental in-tree build (tools/variant.sh); default is the product library
+LIB_PATH = _HERE / os.environ.get("SMM_LIB", "_smm_b200.so")
 
 SMM_OK = 0
 SMM_ERR_INVALID = 1

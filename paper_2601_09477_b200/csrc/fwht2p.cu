@@ -129,6 +129,25 @@ __global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax,
 }
 
 // ------------------------------------------------------------------ kernel
+// x / d for 0 <= x < 2^31 by multiply-high (the scheduler thread decodes an item
+// on the critical path of every CTA barrier; 32-bit division costs ~20 instructions)
+struct FastDiv {
+  uint32_t m, d;
+  int s;
+};
+static FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.s = 0;
+  while ((1ull << f.s) < d) ++f.s;
+  f.m = (uint32_t)((((1ull << f.s) - d) << 32) / d + 1);
+  return f;
+}
+__device__ __forceinline__ int fdiv(int x, const FastDiv &f) {
+  return (int)((__umulhi((uint32_t)x, f.m) + (uint32_t)x) >> f.s);
+}
+__device__ __forceinline__ int fmod_(int x, const FastDiv &f) { return x - fdiv(x, f) * (int)f.d; }
+
 struct TwoPassArgs {
   SketchHashes h;
   const double *X[2];  // k-minor operands: element (i, k) at X[op][i * ld[op] + k]
@@ -136,6 +155,7 @@ struct TwoPassArgs {
   int64_t k0, K;
   int B, hb, d, nblk, ntiles, U, nslot;
   int F, LB, df;  // top-level fold: F = b / 2^LB slices of 2^LB buckets; df = d * F
+  FastDiv div_df, div_F, div_slot;
   const int32_t *off;
   const uint32_t *ent;
   int64_t nmax, bsz;
@@ -261,9 +281,12 @@ __device__ __forceinline__ PullHead pull_head(const TwoPassArgs &p, int t, int o
 __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
                                            double *S, const PullHead &hd) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool kvalid = (int64_t)kappa * KT + lane < p.K;
-  const double *X = p.X[op] + (p.k0 + (int64_t)kappa * KT + lane);
-  const int64_t ld = p.ld[op];
+  // lanes past the end of the inner range read a valid element and are zeroed after the pull
+  const int64_t kk = (int64_t)kappa * KT + lane;
+  const bool full_tile = (int64_t)kappa * KT + KT <= p.K;  // warp-uniform
+  // row address = base + i * (ld * 8): one 32x32->64-bit multiply-add per entry (ld < 2^28)
+  const char *Xb = (const char *)(p.X[op] + p.k0 + (kk < p.K ? kk : p.K - 1));
+  const uint32_t ldb = (uint32_t)(p.ld[op] * 8);
   const int64_t row = (int64_t)t * 2 + op;
   const uint32_t *ent = p.ent + row * p.nmax;
   const int e_lo = hd.e_lo;
@@ -280,7 +303,9 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
     for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
 #pragma unroll
     for (int s = 0; s < 8; ++s)
-      x[s] = (eb + s < e_hi && kvalid) ? __ldg(X + (int64_t)(es[s] & 0x03ffffffu) * ld) : 0.0;
+      x[s] = eb + s < e_hi
+                 ? __ldg((const double *)(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb))
+                 : 0.0;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       if (eb + s < e_hi) {  // warp-uniform
@@ -298,6 +323,10 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
         }
       }
     }
+  }
+  if (!full_tile && kk >= p.K) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.0;
   }
   PROF_MARK(3);
   reg_fwht32(v, 0, 5);  // bucket bits 0-4
@@ -429,12 +458,12 @@ struct Item {
 __device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, int log2g) {
   // prologue: P1 of units 0..LAG-1; then groups g = 0..U-1: [P1(g+LAG) x nblk][P2(g) x nblk]
   // (the P1 part is absent once g+LAG >= U).  2*nblk is a power of two.
-  const int G1 = p.nblk;
+  const int G1 = p.nblk;  // = 2^(log2g - 1)
   const int pro_units = p.U < SMM_LAG ? p.U : SMM_LAG;
   Item it;
   it.pos = pos;
   if (pos < (int64_t)pro_units * G1) {
-    it.is_p1 = 1; it.u = (int)(pos / G1); it.idx = (int)(pos % G1);
+    it.is_p1 = 1; it.u = (int)(pos >> (log2g - 1)); it.idx = (int)(pos & (G1 - 1));
     return it;
   }
   const int q = (int)(pos - (int64_t)pro_units * G1);
@@ -447,7 +476,7 @@ __device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, i
     else { it.is_p1 = 0; it.u = g; it.idx = r - G1; }
   } else {
     const int q2 = q - regular;
-    it.is_p1 = 0; it.u = full + q2 / G1; it.idx = q2 % G1;
+    it.is_p1 = 0; it.u = full + (q2 >> (log2g - 1)); it.idx = q2 & (G1 - 1);
   }
   return it;
 }
@@ -497,7 +526,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     } else {
       if (it.u > ver1) { dep_ptr = done1 + it.u; dep_target = G1; }
     }
-    if (dep_ptr) dep_val = ld_relaxed(dep_ptr);
+    if (dep_ptr) dep_val = ld_acquire(dep_ptr);  // issued an item ahead: its latency is hidden
   };
   if (tid == 0) {
     const int64_t cur = atomicAdd(ticket, 1);
@@ -515,25 +544,31 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     if (tid == 0) {
       const Item it = itn;
       if (dep_ptr) {  // dependency of this item (dispensed earlier: cannot deadlock)
+        const long long w0 = g_prof_on ? clock64() : 0;
         while (dep_val < dep_target) {
           __nanosleep(64);
-          dep_val = ld_relaxed(dep_ptr);
+          dep_val = ld_acquire(dep_ptr);
         }
+        if (g_prof_on) s_prof[it.is_p1 ? 11 : 12] += clock64() - w0;  // informational (inside m0)
         if (it.is_p1) ver2 = it.u - p.nslot;
         else ver1 = it.u;
+        // the counter was observed with acquire loads; barrier [A] extends the order
+        // to the CTA (a counter already observed by an earlier item needs nothing new)
       }
-      __threadfence();  // acquire side of the counters observed above
+      PROF_MARK(13);
       const Item in = decode_item(p, nxt, log2g);
+      const int ut = fmod_(it.u, p.div_df);
+      const int un = fmod_(in.u, p.div_df);
       s_item[0] = it.pos < total ? 1 : 0;
       s_item[1] = it.is_p1;
       s_item[2] = it.u;
       s_item[3] = it.idx;
-      s_item[4] = it.u / p.df;
-      s_item[5] = (it.u % p.df) / p.F;
-      s_item[6] = it.u % p.nslot;
-      s_item[10] = (it.u % p.df) % p.F;
+      s_item[4] = fdiv(it.u, p.div_df);
+      s_item[5] = fdiv(ut, p.div_F);
+      s_item[6] = fmod_(it.u, p.div_slot);
+      s_item[10] = fmod_(ut, p.div_F);
       s_item[7] = (in.pos < total && in.is_p1) ? 1 : 0;
-      s_item[8] = (in.u % p.df) / p.F;
+      s_item[8] = fdiv(un, p.div_F);
       s_item[9] = in.idx;
       itn = in;
     }
@@ -562,8 +597,8 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
     PROF_MARK(10);
     tc_fence_after();
-    if (tid == 32) {  // publish this item's completion
-      __threadfence();
+    if (tid == 32) {  // publish this item's completion (release: covers the CTA's writes via [B])
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       if (is_p1) red_add(done1 + u, 1);
       else {
         red_add(acc_cnt + (t * p.F + asl) * p.nblk + idx, 1);
@@ -623,6 +658,10 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   const int64_t bs = (int64_t)1 << LB;
   const int64_t K = k1 - k0;
   const int64_t nmax = n1 > n2 ? n1 : n2;
+  if (lda >= ((int64_t)1 << 28) || ldb >= ((int64_t)1 << 28)) {  // row offsets are 32-bit byte strides
+    set_error("operand row stride too large for the two-pass kernel");
+    return SMM_ERR_INVALID;
+  }
   if (ws_bytes < fwht2p_workspace(d, log2b, n1, n2, K)) {
     set_error("compress workspace too small (two-pass)");
     return SMM_ERR_WORKSPACE;
@@ -688,6 +727,9 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.ntiles = (int)ntiles;
   p.U = (int)U;
   p.nslot = nslot;
+  p.div_df = make_fastdiv((uint32_t)(d * F));
+  p.div_F = make_fastdiv((uint32_t)F);
+  p.div_slot = make_fastdiv((uint32_t)nslot);
   p.off = off;
   p.ent = ent;
   p.nmax = nmax;
@@ -726,7 +768,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     long long h[16];
     cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost);
     double tot = 0;
-    for (int k = 0; k < 16; ++k) tot += (double)h[k];
+    for (int k = 0; k < 16; ++k)
+      if (k != 11 && k != 12) tot += (double)h[k];  // m11 / m12: dependency waits inside m13
     fprintf(stderr, "[fwht2p profile, %% of thread-0 cycles over all CTAs]");
     for (int k = 0; k < 16; ++k)
       if (h[k]) fprintf(stderr, " m%d=%.1f", k, 100.0 * (double)h[k] / tot);

@@ -77,7 +77,8 @@ def test_hash_tables_match_oracle_on_config_sizes():
 
 
 CONFIGS = ["cfg1", "cfg2", "cfg3", "cfg5_b12_d3_nnz512_fwht", "cfg5_b12_d9_nnz512_fft", "cfg5_b14_d5_nnz512_fwht",
-           "cfg5_b14_d3_nnz512_fft", "cfg5_b16_d9_nnz512_fwht", "cfg5_b16_d5_nnz512_fft"]
+           "cfg5_b14_d3_nnz512_fft", "cfg5_b16_d9_nnz512_fwht", "cfg5_b16_d5_nnz512_fft",
+           "cfg5_b18_d3_nnz512_fwht", "cfg5_b18_d3_nnz512_fft", "cfg5_b20_d3_nnz512_fwht", "cfg5_b20_d3_nnz512_fft"]
 
 
 @pytest.mark.parametrize("name", CONFIGS)
