@@ -28,6 +28,9 @@
  *   smm_fwht_batched         transforms.py:37-49 / 100-127 (fwht_inplace, xor_convolve)
  *   smm_fft_batched          transforms.py:52-74 / 130-175 (fft_forward, fft_inverse,
  *                            cyclic_convolve)
+ *   smm_copy2d               np.ascontiguousarray(a, dtype=float64) (sketch.py:282-286):
+ *                            the host->device move of the operands, done per k-slab so
+ *                            uploads overlap the compress kernel
  */
 #ifndef SKETCHMM_B200_H
 #define SKETCHMM_B200_H
@@ -48,6 +51,12 @@ extern "C" {
 #define SMM_VARIANT_FWHT 1
 
 #define SMM_MAX_DEPTH 63
+
+/* OR into `variant` of the compress entry points: acc is ADDED to instead of
+ * overwritten.  With the two-pass FWHT kernel and k-ranges split on multiples of
+ * 32, consecutive calls reproduce one call's summation order bit for bit
+ * (host-streamed operands: each slab is uploaded while the previous computes). */
+#define SMM_FLAG_ACCUMULATE 0x100
 
 #define SMM_LAYOUT_KMAJOR 0
 #define SMM_LAYOUT_KMINOR 1
@@ -90,6 +99,12 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
                                const double *b, int64_t ldb, int b_layout, int64_t n1, int64_t n2,
                                int64_t k0, int64_t k1, const uint64_t *words_host, int d, int log2b,
                                void *acc, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Strided 2-D copy between any host/device pointers (cudaMemcpyDefault) on
+ * `stream`: `rows` rows of width_bytes, pitches in bytes.  Used to stream a
+ * k-slab of a host-resident row-major A (a column block) to the device. */
+int smm_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t rows,
+               void *stream);
 
 /* Step 4: polys [dev] (d x b float64) = inverse transform of acc, times 1/b. */
 int smm_finalize(int variant, const void *acc, double *polys, int d, int log2b, void *stream);

@@ -97,11 +97,12 @@ def _rowmajor(x: torch.Tensor) -> torch.Tensor:
 
 def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str,
                         k0: int, k1: int, acc: torch.Tensor | None = None, a_layout: int = KMAJOR,
-                        b_layout: int = KMAJOR) -> torch.Tensor:
+                        b_layout: int = KMAJOR, accumulate: bool = False) -> torch.Tensor:
     """Pre-inverse accumulator of inner indices [k0, k1).
 
     ``a`` is A^T (KMAJOR, rows = k) or A itself (KMINOR, columns = k); ``b`` is B
     (KMAJOR) or B^T (KMINOR).  Views with a row stride are used in place.
+    ``accumulate`` adds to ``acc`` instead of overwriting it (SMM_FLAG_ACCUMULATE).
     """
     lib = _lib.load()
     a = _rowmajor(a)
@@ -110,6 +111,10 @@ def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: 
     n1 = a.shape[1] if a_layout == KMAJOR else a.shape[0]
     n2 = b.shape[1] if b_layout == KMAJOR else b.shape[0]
     v = _lib.VARIANT[variant]
+    if accumulate:
+        if acc is None:
+            raise InvalidParameterError("accumulate=True needs an accumulator to add to")
+        v |= _lib.FLAG_ACCUMULATE
     nbytes = ctypes.c_int64(0)
     _lib.check(lib.smm_compress_workspace_ex(v, d, log2b, n1, n2, k0, k1, a_layout, b_layout, ctypes.byref(nbytes)))
     ws = workspace(nbytes.value, dev)
@@ -119,6 +124,97 @@ def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: 
     _lib.check(lib.smm_compress_accumulate_ex(v, ptr(a), a.stride(0), a_layout, ptr(b), b.stride(0), b_layout, n1,
                                               n2, k0, k1, wp, d, log2b, ptr(acc), ptr(ws), ws.numel(),
                                               stream_ptr(dev)))
+    return acc
+
+
+def copy2d(dst: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream) -> None:
+    """dst[...] = src for 2-D row-strided views (host or device, any direction) on ``stream``."""
+    lib = _lib.load()
+    if dst.shape != src.shape or dst.dtype != src.dtype or dst.stride(1) != 1 or src.stride(1) != 1:
+        raise InvalidParameterError("copy2d needs equal-shape row-strided views")
+    es = src.element_size()
+    _lib.check(lib.smm_copy2d(ptr(dst), dst.stride(0) * es, ptr(src), src.stride(0) * es, src.shape[1] * es,
+                              src.shape[0], ctypes.c_void_p(stream.cuda_stream)))
+
+
+def host_f64(x) -> torch.Tensor:
+    """A host operand as a row-strided float64 CPU tensor (no copy when it already is one)."""
+    if isinstance(x, torch.Tensor):
+        t = x if x.dtype == torch.float64 else x.to(torch.float64)
+    else:
+        t = torch.from_numpy(np.asarray(x, dtype=np.float64))
+    if t.dim() != 2:
+        raise InvalidParameterError("operands must be 2-D")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    return t
+
+
+def stream_chunk(m: int, n_max: int) -> int:
+    """k-slab width for host-streamed compress: ~8 slabs, a multiple of 32 (k-tile aligned)."""
+    kc = max(256, -(-m // 8))
+    kc = -(-kc // 32) * 32
+    # keep one slab of both operands under ~1 GiB
+    while kc > 256 and 8 * kc * n_max * 2 > (1 << 30):
+        kc //= 2
+    return max(32, min(kc, -(-m // 32) * 32))
+
+
+def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str,
+                  a_layout: int, device: torch.device, chunk: int | None = None) -> torch.Tensor:
+    """Pre-inverse accumulator of host-resident operands, streamed in k-slabs.
+
+    Slab c+1 is uploaded on a copy stream (2-D copies: a k-slab of a row-major A is
+    a column block) while the kernel accumulates slab c; every slab after the first
+    is added in SMM_FLAG_ACCUMULATE mode, so with the two-pass FWHT kernel the
+    result is bit-identical to one call over the whole inner range.
+    """
+    m = a.shape[1] if a_layout == KMINOR else a.shape[0]
+    n1 = a.shape[0] if a_layout == KMINOR else a.shape[1]
+    n2 = b.shape[1]
+    if b.shape[0] != m:
+        raise InvalidParameterError(f"inner dimensions must match, got {m} and {b.shape[0]}")
+    kc = chunk or stream_chunk(m, max(n1, n2))
+    acc = torch.empty(acc_shape(variant, d, 1 << log2b), dtype=torch.float64, device=device)
+    if m == 0:
+        return compress_accumulate(torch.empty((0, n1) if a_layout == KMAJOR else (n1, 0), dtype=torch.float64,
+                                               device=device), torch.empty((0, n2), dtype=torch.float64, device=device),
+                                   words, d, log2b, variant, 0, 0, acc, a_layout, KMAJOR)
+    compute = torch.cuda.current_stream(device)
+    copy = torch.cuda.Stream(device)
+    abuf = [torch.empty((n1, kc) if a_layout == KMINOR else (kc, n1), dtype=torch.float64, device=device)
+            for _ in range(2)]
+    bbuf = [torch.empty((kc, n2), dtype=torch.float64, device=device) for _ in range(2)]
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    slabs = [(c0, min(m, c0 + kc)) for c0 in range(0, m, kc)]
+
+    def upload(c):
+        c0, c1 = slabs[c]
+        w = c1 - c0
+        q = c % 2
+        with torch.cuda.stream(copy):
+            if c >= 2:
+                copy.wait_event(freed[q])
+            if a_layout == KMINOR:
+                copy2d(abuf[q][:, :w], a[:, c0:c1], copy)
+            else:
+                copy2d(abuf[q][:w], a[c0:c1], copy)
+            copy2d(bbuf[q][:w], b[c0:c1], copy)
+            loaded[q].record(copy)
+
+    upload(0)
+    for c, (c0, c1) in enumerate(slabs):
+        if c + 1 < len(slabs):
+            upload(c + 1)
+        q = c % 2
+        w = c1 - c0
+        compute.wait_event(loaded[q])
+        av = abuf[q][:, :w] if a_layout == KMINOR else abuf[q][:w]
+        compress_accumulate(av, bbuf[q][:w], words, d, log2b, variant, 0, w, acc, a_layout, KMAJOR,
+                            accumulate=c > 0)
+        freed[q].record(compute)
+    compute.wait_stream(copy)
     return acc
 
 
@@ -157,6 +253,47 @@ def extract(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant:
             # the bitmask of this extract call is still in `ws`: emit pairs without recomputing medians
             _lib.check(lib.smm_hh_pairs(ptr(ws), n2, r0, r1, ptr(pairs), cnt, stream_ptr(dev)))
     return est, count, pairs
+
+
+def extract_host(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str, n1: int, n2: int,
+                 r0: int, r1: int, thr: float, strict: bool, est_host: torch.Tensor, block_rows: int | None = None):
+    """Rows [r0, r1) of the estimates into a host tensor, in row blocks: block q+1
+    is extracted while block q is copied out on a copy stream (2-slot device ring).
+    Returns the heavy-hitter pairs as a pinned host tensor; both are complete on return."""
+    dev = polys.device
+    rows = r1 - r0
+    if tuple(est_host.shape) != (rows, n2) or est_host.dtype != torch.float64 or est_host.stride(1) != 1:
+        raise InvalidParameterError(f"est_out must be a ({rows}, {n2}) float64 row-major tensor")
+    if rows == 0 or n2 == 0:
+        _, _, pairs = extract(polys, words, d, log2b, variant, n1, n2, r0, r1, want_est=False, thr=thr,
+                              strict=strict, want_pairs=True)
+        return pairs.cpu()
+    R = block_rows or max(1, min(rows, (128 << 20) // (8 * n2)))
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    ring = [torch.empty((R, n2), dtype=torch.float64, device=dev) for _ in range(min(2, -(-rows // R)))]
+    ready = [torch.cuda.Event() for _ in ring]
+    done = [torch.cuda.Event() for _ in ring]
+    pairs = []
+    for bi, q0 in enumerate(range(r0, r1, R)):
+        q1 = min(r1, q0 + R)
+        slot = bi % len(ring)
+        if bi >= len(ring):
+            compute.wait_event(done[slot])
+        _, _, pr = extract(polys, words, d, log2b, variant, n1, n2, q0, q1, want_est=True, thr=thr, strict=strict,
+                           want_pairs=True, est_out=ring[slot][:q1 - q0])
+        pairs.append(pr)
+        ready[slot].record(compute)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ready[slot])
+            copy2d(est_host[q0 - r0:q1 - r0], ring[slot][:q1 - q0], copy)
+            done[slot].record(copy)
+    pairs = torch.cat(pairs) if len(pairs) > 1 else pairs[0]
+    pairs_host = torch.empty(pairs.shape, dtype=pairs.dtype, pin_memory=True)
+    pairs_host.copy_(pairs, non_blocking=True)  # on the compute stream, behind the last extraction
+    compute.wait_stream(copy)
+    compute.synchronize()
+    return pairs_host
 
 
 def fwht_batched(x: torch.Tensor, scale: float = 1.0) -> torch.Tensor:

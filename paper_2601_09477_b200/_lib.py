@@ -23,6 +23,7 @@ SMM_ERR_CUDA = 2
 SMM_ERR_WORKSPACE = 3
 VARIANT = {"fft": 0, "fwht": 1}
 MAX_DEPTH = 63
+FLAG_ACCUMULATE = 0x100
 
 EXPORTS = (
     "smm_abi_version",
@@ -38,6 +39,7 @@ EXPORTS = (
     "smm_hh_pairs",
     "smm_kernel_launches",
     "smm_transpose",
+    "smm_copy2d",
     "smm_fwht_batched",
     "smm_fft_batched",
 )
@@ -82,6 +84,7 @@ def load():
             "smm_hh_pairs": ([P, I64, I64, I64, P, I64, P], I),
             "smm_kernel_launches": ([], I64),
             "smm_transpose": ([P, I64, I64, I64, P, I64, P], I),
+            "smm_copy2d": ([P, I64, P, I64, I64, I64, P], I),
             "smm_fwht_batched": ([P, I64, I, D, P], I),
             "smm_fft_batched": ([P, I64, I, I, D, P], I),
         }

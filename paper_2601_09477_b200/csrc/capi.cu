@@ -11,8 +11,9 @@ int64_t fft_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K, int G
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2);
 int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K);
 int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb,
-                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
-                      cudaStream_t s);
+                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws,
+                      int64_t ws_bytes, cudaStream_t s);
+int add_inplace(double *dst, const double *src, int64_t n, cudaStream_t s);
 int fwht_accumulate(const SketchHashes &h, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm,
                     int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
                     cudaStream_t s);
@@ -41,6 +42,12 @@ using namespace smm;
       return SMM_ERR_INVALID;    \
     }                            \
   } while (0)
+
+// bytes of one pre-inverse accumulator
+static int64_t acc_bytes(int variant, int d, int log2b) {
+  const int64_t b = (int64_t)1 << log2b;
+  return variant == SMM_VARIANT_FWHT ? (int64_t)d * b * 8 : (int64_t)d * (b / 2 + 1) * 16;
+}
 
 static int check_sketch(int variant, int d, int log2b) {
   SMM_REQUIRE(variant == SMM_VARIANT_FFT || variant == SMM_VARIANT_FWHT, "unknown transform variant %d", variant);
@@ -76,15 +83,18 @@ int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int
 // contiguous); the fold kernels (FFT, small/large b) read k-major rows.  An
 // operand in the other layout is transposed (only its [k0, k1) slab) into the
 // front of the workspace.
+// SMM_FLAG_ACCUMULATE: the two-pass kernel continues the k order in acc itself;
+// the other kernels reduce into a workspace accumulator that is then added.
 struct CompressPlan {
-  bool two_pass;
+  bool two_pass, acc_add;
   bool ta, tb;  // transpose A / B slab
-  int64_t ta_bytes, tb_bytes, kernel_bytes;
+  int64_t ta_bytes, tb_bytes, tmp_acc_bytes, kernel_bytes;
 };
 
 static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t K, int alay,
-                                  int blay) {
+                                  int blay, bool acc_add) {
   CompressPlan c;
+  c.acc_add = acc_add;
   c.two_pass = variant == SMM_VARIANT_FWHT && fwht2p_supported(log2b, n1, n2);
   const int want = c.two_pass ? SMM_LAYOUT_KMINOR : SMM_LAYOUT_KMAJOR;
   c.ta = alay != want;
@@ -94,18 +104,21 @@ static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int
   if (c.two_pass) c.kernel_bytes = fwht2p_workspace(d, log2b, n1, n2, K);
   else if (variant == SMM_VARIANT_FWHT) c.kernel_bytes = fwht_workspace(d, log2b, n1, n2, K, num_sms());
   else c.kernel_bytes = fft_workspace(d, log2b, n1, n2, K, num_sms());
+  c.tmp_acc_bytes = (acc_add && !c.two_pass) ? ((acc_bytes(variant, d, log2b) + 255) / 256) * 256 : 0;
   return c;
 }
 
 int smm_compress_workspace_ex(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
                               int a_layout, int b_layout, int64_t *bytes) {
+  const bool acc_add = (variant & SMM_FLAG_ACCUMULATE) != 0;
+  variant &= ~SMM_FLAG_ACCUMULATE;
   int rc = check_sketch(variant, d, log2b);
   if (rc) return rc;
   SMM_REQUIRE(bytes != nullptr, "bytes is NULL");
   SMM_REQUIRE(n1 >= 0 && n2 >= 0 && k0 >= 0 && k1 >= k0, "bad shapes");
   SMM_REQUIRE((a_layout == 0 || a_layout == 1) && (b_layout == 0 || b_layout == 1), "bad layout");
-  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, k1 - k0, a_layout, b_layout);
-  *bytes = c.ta_bytes + c.tb_bytes + c.kernel_bytes;
+  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, k1 - k0, a_layout, b_layout, acc_add);
+  *bytes = c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes + c.kernel_bytes;
   return SMM_OK;
 }
 
@@ -118,6 +131,8 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
                                int b_layout, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
                                const uint64_t *words_host, int d, int log2b, void *acc, void *workspace,
                                int64_t workspace_bytes, void *stream) {
+  const bool acc_add = (variant & SMM_FLAG_ACCUMULATE) != 0;
+  variant &= ~SMM_FLAG_ACCUMULATE;
   int rc = check_sketch(variant, d, log2b);
   if (rc) return rc;
   SMM_REQUIRE(words_host != nullptr && acc != nullptr, "NULL argument");
@@ -131,12 +146,13 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
   load_hashes(h, words_host, d, log2b);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t K = k1 - k0;
-  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, K, a_layout, b_layout);
-  if (workspace_bytes < c.ta_bytes + c.tb_bytes + c.kernel_bytes) {
-    set_error("compress workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
-              (long long)(c.ta_bytes + c.tb_bytes + c.kernel_bytes));
+  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, K, a_layout, b_layout, acc_add);
+  const int64_t need = c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes + c.kernel_bytes;
+  if (workspace_bytes < need) {
+    set_error("compress workspace too small: %lld < %lld bytes", (long long)workspace_bytes, (long long)need);
     return SMM_ERR_WORKSPACE;
   }
+  if (acc_add && K == 0) return SMM_OK;
   char *ws = (char *)workspace;
   // operand views in the layout the chosen kernel reads; offsets so that inner index k0 maps to x[.. + k0]
   const double *xa = a, *xb = b;
@@ -165,12 +181,27 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
     xb = t;
     lb = c.two_pass ? K : n2;
   }
-  char *kws = ws + c.ta_bytes + c.tb_bytes;
-  const int64_t kb = workspace_bytes - c.ta_bytes - c.tb_bytes;
-  if (c.two_pass) return fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, kws, kb, s);
+  char *kws = ws + c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes;
+  const int64_t kb = workspace_bytes - c.ta_bytes - c.tb_bytes - c.tmp_acc_bytes;
+  if (c.two_pass) return fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, acc_add, kws, kb, s);
+  void *dst = acc_add ? (void *)(ws + c.ta_bytes + c.tb_bytes) : acc;
   if (variant == SMM_VARIANT_FWHT)
-    return fwht_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, kws, kb, s);
-  return fft_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (cplx *)acc, kws, kb, s);
+    rc = fwht_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)dst, kws, kb, s);
+  else
+    rc = fft_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (cplx *)dst, kws, kb, s);
+  if (rc || !acc_add) return rc;
+  return add_inplace((double *)acc, (const double *)dst, acc_bytes(variant, d, log2b) / 8, s);
+}
+
+int smm_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t rows,
+               void *stream) {
+  SMM_REQUIRE(width_bytes >= 0 && rows >= 0 && dpitch >= width_bytes && spitch >= width_bytes, "bad copy shape");
+  SMM_REQUIRE(width_bytes == 0 || rows == 0 || (dst != nullptr && src != nullptr), "NULL argument");
+  if (width_bytes == 0 || rows == 0) return SMM_OK;
+  SMM_CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes, (size_t)rows,
+                                 cudaMemcpyDefault, (cudaStream_t)stream),
+               "cudaMemcpy2DAsync");
+  return SMM_OK;
 }
 
 int smm_compress_accumulate(int variant, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm, int64_t n1,

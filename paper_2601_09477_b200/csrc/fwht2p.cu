@@ -163,6 +163,7 @@ struct TwoPassArgs {
   double *acc; // [d][b]
   int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
   long long *prof;  // [16] phase cycles (nullable)
+  int acc_add;      // add to acc (continue an earlier call's k order) instead of overwriting it
 };
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -377,7 +378,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)(sg_acc & hmask) * 256 + lo0 + (sg_acc >> hb);
   // usually the previous k-tile's update of this slice finished long ago: fetch the old value early
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
-  const double acc_old = (kappa > 0 && acc_ready) ? __ldcg(a) : 0.0;
+  const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * wq) << 16);
   const uint32_t col_fa = (uint32_t)(wh * 64);
   double v[32];
@@ -436,7 +437,8 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
 #pragma unroll
   for (int j = 0; j < 32; ++j) sum += W[lane * 32 + (j ^ lane)];
   if (kappa == 0) {
-    __stcg(a, sum);
+    // accumulate mode continues a previous call's k order exactly (chunk boundaries are k-tiles)
+    __stcg(a, p.acc_add ? acc_old + sum : sum);
   } else if (acc_ready) {
     __stcg(a, acc_old + sum);
   } else {
@@ -649,8 +651,8 @@ int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
 }
 
 int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb,
-                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
-                      cudaStream_t s) {
+                      int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws,
+                      int64_t ws_bytes, cudaStream_t s) {
   const int d = h.d, log2b = h.log2b;
   int LB, F;
   fwht2p_geometry(log2b, LB, F);
@@ -681,7 +683,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   const int64_t U = ntiles * d * F;
   const int nblk = (int)(bs >> P1_BITS);
   if (K <= 0) {
-    SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
+    if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
     return SMM_OK;
   }
   if (U > (int64_t)1 << 30) {
@@ -738,6 +740,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.acc = acc;
   p.ctr = ctr;
   p.prof = nullptr;
+  p.acc_add = acc_add ? 1 : 0;
   static const bool prof_on = getenv("SMM_PROFILE") != nullptr;
   if (prof_on) {
     cudaMalloc((void **)&p.prof, 16 * sizeof(long long));

@@ -142,6 +142,21 @@ __global__ void copy_kernel(const double *src, double *dst, int64_t n) {
     dst[q] = src[q];
 }
 
+__global__ void add_kernel(double *dst, const double *src, int64_t n) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    dst[q] += src[q];
+}
+
+// dst += src (n doubles): accumulate mode of the kernels that reduce their partials at the end
+int add_inplace(double *dst, const double *src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return SMM_OK;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > 4 * 148 * 8) blocks = 4 * 148 * 8;
+  add_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, n);
+  SMM_LAUNCH_CHECK("add_kernel");
+  return SMM_OK;
+}
+
 // z[t][u] = acc[t][u] (u <= b/2), z[t][b-u] = conj(acc[t][u]) (1 <= u < b/2): sketch.py:227-231
 __global__ void hermitian_fill_kernel(const cplx *acc, cplx *z, int d, int log2b) {
   const int64_t b = (int64_t)1 << log2b, half = b / 2 + 1;

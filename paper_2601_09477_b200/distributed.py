@@ -52,8 +52,13 @@ def compress_sharded(a_slab, b_slab, params: SketchParams, n_rows: int | None = 
     if kl != b_slab.shape[0]:
         raise InvalidParameterError(f"inner slabs must match, got {kl} and {b_slab.shape[0]}")
     hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
-    acc = _device.compress_accumulate(a_slab, b_slab, hashes.packed_words(), params.d, params.log2b,
-                                      params.transform, 0, kl, a_layout=a_layout)
+    if not getattr(a_slab, "is_cuda", False) and not getattr(b_slab, "is_cuda", False):
+        # host slabs: streamed upload overlapped with the compress kernel
+        acc = _device.compress_host(_device.host_f64(a_slab), _device.host_f64(b_slab), hashes.packed_words(),
+                                    params.d, params.log2b, params.transform, a_layout, _device.require_cuda())
+    else:
+        acc = _device.compress_accumulate(a_slab, b_slab, hashes.packed_words(), params.d, params.log2b,
+                                          params.transform, 0, kl, a_layout=a_layout)
     reduce_accumulator(acc, group=group, all_reduce=all_reduce)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)
     return ProductSketch(polys=polys, hashes=hashes, params=params,

@@ -219,6 +219,38 @@ def _run(a, b, params: SketchParams, threads, a_layout: int, b_layout: int = 0) 
     return ProductSketch(polys=polys, hashes=hashes, params=params, n_rows=n_rows, n_cols=b.shape[1])
 
 
+def _is_host(m) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(m, torch.Tensor):
+        return not m.is_cuda
+    return True  # numpy arrays and nested sequences live on the host
+
+
+def _run_host(a, b, params: SketchParams, threads, a_layout: int, dev) -> ProductSketch:
+    """_run for host-resident operands: k-slabs are uploaded while earlier slabs
+    compute (pinned host tensors give the full PCIe rate)."""
+    from . import _device
+
+    a = _device.host_f64(a)
+    b = _device.host_f64(b)
+    effective_threads(threads)
+    hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
+    _check_depth(params)
+    acc = _device.compress_host(a, b, hashes.packed_words(), params.d, params.log2b, params.transform, a_layout, dev)
+    polys = _device.finalize(acc, params.d, params.log2b, params.transform)
+    n_rows = a.shape[0] if a_layout == _device.KMINOR else a.shape[1]
+    return ProductSketch(polys=polys, hashes=hashes, params=params, n_rows=n_rows, n_cols=b.shape[1])
+
+
+def _dispatch(a, b, params, threads, a_layout, dev, what_a):
+    if _is_host(a) and _is_host(b):
+        return _run_host(a, b, params, threads, a_layout, dev)
+    return _run(_as_matrix(a, what_a, dev), _as_matrix(b, "right operand", dev), params, threads, a_layout)
+
+
 def _check_depth(params: SketchParams) -> None:
     from ._lib import MAX_DEPTH
 
@@ -237,8 +269,7 @@ def compress(a, b, params: SketchParams, threads: int | None = None, device=None
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    return _run(_as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev), params, threads,
-                _device.KMINOR)
+    return _dispatch(a, b, params, threads, _device.KMINOR, dev, "left operand")
 
 
 def compress_pretransposed(at, b, params: SketchParams, threads: int | None = None, device=None) -> ProductSketch:
@@ -252,8 +283,7 @@ def compress_pretransposed(at, b, params: SketchParams, threads: int | None = No
         raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    return _run(_as_matrix(at, "left operand (transposed)", dev), _as_matrix(b, "right operand", dev), params,
-                threads, _device.KMAJOR)
+    return _dispatch(at, b, params, threads, _device.KMAJOR, dev, "left operand (transposed)")
 
 
 def compress_rect(a, b, params: SketchParams, threads: int | None = None, device=None) -> ProductSketch:
@@ -266,8 +296,7 @@ def compress_rect(a, b, params: SketchParams, threads: int | None = None, device
         raise InvalidParameterError(f"inner dimension must equal params.n={params.n}, got {sa} x {sb}")
     effective_threads(threads)
     dev = _device.require_cuda(device)
-    return _run(_as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev), params, threads,
-                _device.KMINOR)
+    return _dispatch(a, b, params, threads, _device.KMINOR, dev, "left operand")
 
 
 # ----------------------------------------------------------------------------- decompress
@@ -354,7 +383,9 @@ def heavy_hitters(sketch: ProductSketch, threshold: float = 0.5, strict: bool = 
 def extract_all(sketch: ProductSketch, threshold: float = 0.5, strict: bool = True, *, r0: int = 0,
                 r1: int | None = None, device=None, est_out=None):
     """Step 5 in one pass: the estimate rows [r0, r1) and their heavy-hitter pairs
-    (CUDA tensors).  This is ``decompress_all`` fused with the threshold."""
+    (CUDA tensors).  This is ``decompress_all`` fused with the threshold.  With a
+    host ``est_out`` the rows are streamed out in blocks and the pairs come back as
+    a pinned host tensor; both are complete on return."""
     from . import _device
 
     r1 = sketch.n_rows if r1 is None else r1
@@ -362,6 +393,11 @@ def extract_all(sketch: ProductSketch, threshold: float = 0.5, strict: bool = Tr
         raise InvalidParameterError(f"row range [{r0}, {r1}) outside {sketch.n_rows} rows")
     p = sketch.params
     polys = sketch.polys_device(device)
+    if est_out is not None and not est_out.is_cuda:
+        # host destination (pinned for full speed): extraction of row block q+1 overlaps the copy-out of q
+        pairs = _device.extract_host(polys, sketch.words, p.d, p.log2b, p.transform, sketch.n_rows, sketch.n_cols,
+                                     r0, r1, threshold, strict, est_out)
+        return est_out, pairs
     est, _, pairs = _device.extract(polys, sketch.words, p.d, p.log2b, p.transform, sketch.n_rows, sketch.n_cols,
                                     r0, r1, want_est=True, thr=threshold, strict=strict, want_pairs=True,
                                     est_out=est_out)

@@ -260,3 +260,62 @@ def test_transforms_api(transforms_golden):
         P.fft_inverse([1 + 1e-3j, 0, 1])
     with pytest.raises(P.InvalidParameterError):
         P.fwht_inplace(np.zeros(6))
+
+
+@pytest.mark.parametrize("transform,log2b", [("fwht", 12), ("fwht", 6), ("fft", 10)])
+def test_host_streamed_compress(transform, log2b):
+    # host operands are uploaded in k-slabs while earlier slabs compute; every slab
+    # after the first runs in accumulate mode.  The two-pass FWHT kernel continues
+    # the single call's k order exactly; the other kernels add a slab accumulator.
+    rng = np.random.default_rng(7)
+    n1, m, n2 = 700, 1000, 650
+    a = rng.standard_normal((n1, m))
+    b = rng.standard_normal((m, n2))
+    words = O.draw_words(11, 5, 1 << log2b)
+    dev = torch.device("cuda")
+    ref = _device.compress_accumulate(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), words, 5, log2b,
+                                      transform, 0, m, a_layout=_device.KMINOR, b_layout=_device.KMAJOR)
+    a_h = torch.from_numpy(a).pin_memory()
+    b_h = torch.from_numpy(b).pin_memory()
+    for chunk in (64, 96, 1024):
+        got = _device.compress_host(a_h, b_h, words, 5, log2b, transform, _device.KMINOR, dev, chunk=chunk)
+        if transform == "fwht" and log2b >= 8:
+            assert torch.equal(got, ref)
+        else:
+            scale = float(ref.abs().max())
+            assert float((got - ref).abs().max()) <= 1e-12 * scale
+    # A^T given (k-major): the k-slab is a row block of the host array
+    at_h = torch.from_numpy(np.ascontiguousarray(a.T))
+    got = _device.compress_host(at_h, b_h, words, 5, log2b, transform, _device.KMAJOR, dev, chunk=128)
+    scale = float(ref.abs().max())
+    assert float((got - ref).abs().max()) <= 1e-12 * scale
+
+
+def test_public_api_host_operands_bitwise_equal_to_device_operands():
+    w = W.make("cfg1", xp=torch, device="cuda")
+    p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+    dev_sk = P.compress(w.a, w.bmat, p)
+    host_sk = P.compress(w.a.cpu().pin_memory(), w.bmat.cpu(), p)
+    np_sk = P.compress(w.a.cpu().numpy(), w.bmat.cpu().numpy(), p)
+    assert np.array_equal(dev_sk.polys, host_sk.polys)
+    assert np.array_equal(dev_sk.polys, np_sk.polys)
+
+
+def test_extract_to_host_matches_device():
+    w = W.make("cfg1", xp=torch, device="cuda")
+    p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+    sk = P.compress(w.a, w.bmat, p)
+    est_d, pairs_d = P.extract_all(sk, w.threshold, strict=True)
+    host = torch.empty((w.n, w.n), dtype=torch.float64).pin_memory()
+    est_h, pairs_h = P.extract_all(sk, w.threshold, strict=True, est_out=host)
+    assert est_h is host
+    assert torch.equal(est_h, est_d.cpu())
+    assert not pairs_h.is_cuda and pairs_h.is_pinned()
+    assert torch.equal(pairs_h, pairs_d.cpu())
+    # small row blocks exercise the 2-slot ring
+    host2 = torch.empty((300, w.n), dtype=torch.float64)
+    pairs2 = _device.extract_host(sk.polys_device(), sk.words, p.d, p.log2b, p.transform, w.n, w.n, 100, 400,
+                                  w.threshold, True, host2, block_rows=37)
+    assert torch.equal(host2, est_d[100:400].cpu())
+    sel = (pairs_d[:, 0] >= 100) & (pairs_d[:, 0] < 400)
+    assert torch.equal(pairs2, pairs_d[sel].cpu())
