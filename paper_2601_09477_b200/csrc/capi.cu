@@ -49,10 +49,12 @@ static int64_t acc_bytes(int variant, int d, int log2b) {
   return variant == SMM_VARIANT_FWHT ? (int64_t)d * b * 8 : (int64_t)d * (b / 2 + 1) * 16;
 }
 
-static int check_sketch(int variant, int d, int log2b) {
+// Compress / finalize accept any depth (stacked repetitions of several seeds);
+// extraction needs an odd d (the median is the middle order statistic).
+static int check_sketch(int variant, int d, int log2b, bool need_odd = false) {
   SMM_REQUIRE(variant == SMM_VARIANT_FFT || variant == SMM_VARIANT_FWHT, "unknown transform variant %d", variant);
-  SMM_REQUIRE(d >= 1 && d % 2 == 1 && d <= SMM_MAX_DEPTH, "d must be an odd integer in [1, %d], got %d",
-              SMM_MAX_DEPTH, d);
+  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH, "d must be in [1, %d], got %d", SMM_MAX_DEPTH, d);
+  SMM_REQUIRE(!need_odd || d % 2 == 1, "d must be an odd integer in [1, %d], got %d", SMM_MAX_DEPTH, d);
   SMM_REQUIRE(log2b >= 1 && log2b <= 32, "b must be a power of two in [2, 2**32], got 2**%d", log2b);
   if (variant == SMM_VARIANT_FFT) SMM_REQUIRE(log2b <= 30, "fft variant supports b <= 2**30");
   return SMM_OK;
@@ -231,7 +233,7 @@ int smm_extract(int variant, const double *polys, const uint64_t *words_host, in
                 int64_t n2, int64_t r0, int64_t r1, double *est, int64_t ld_est, double thr, int strict,
                 int64_t *hh_pairs, int64_t hh_cap, int64_t *hh_count, void *workspace, int64_t workspace_bytes,
                 void *stream) {
-  int rc = check_sketch(variant, d, log2b);
+  int rc = check_sketch(variant, d, log2b, true);
   if (rc) return rc;
   SMM_REQUIRE(polys != nullptr && words_host != nullptr && hh_count != nullptr, "NULL argument");
   SMM_REQUIRE(r0 >= 0 && r1 >= r0 && r1 <= n1 && n2 >= 0, "row range [%lld, %lld) outside %lld rows", (long long)r0,

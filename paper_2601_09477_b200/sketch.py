@@ -299,6 +299,56 @@ def compress_rect(a, b, params: SketchParams, threads: int | None = None, device
     return _dispatch(a, b, params, threads, _device.KMINOR, dev, "left operand")
 
 
+def compress_seeds(a, b, params: SketchParams, seeds, threads: int | None = None, device=None) -> list:
+    """Independent sketches of one product for many hash seeds, batched.
+
+    The reference's Monte-Carlo drivers (variance_experiment / correctness_run,
+    experiments.py:216-312) call ``compress`` once per seed.  Here the seeds'
+    repetitions are stacked into one deeper sketch (up to 63 repetitions per
+    launch), so each operand slab is read once for all of them; every repetition
+    is computed exactly as in its own ``compress`` call, so sketch ``s`` equals
+    ``compress(a, b, replace(params, seed=seeds[s]))``.
+    """
+    from dataclasses import replace
+
+    from . import _device
+    from ._lib import MAX_DEPTH
+
+    seeds = [int(x) for x in seeds]
+    sa = _check_2d(a, "left operand")
+    sb = _check_2d(b, "right operand")
+    n = params.n
+    if sa != (n, n) or sb != (n, n):
+        raise InvalidParameterError(f"operands must both be {n} x {n}, got {sa} and {sb}")
+    per = [replace(params, seed=s) for s in seeds]  # validates every seed
+    effective_threads(threads)
+    dev = _device.require_cuda(device)
+    host = _is_host(a) and _is_host(b)
+    if host:
+        a_op, b_op = _device.host_f64(a), _device.host_f64(b)
+    else:
+        a_op, b_op = _as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev)
+    d = params.d
+    group = max(1, MAX_DEPTH // d)
+    out = []
+    for g0 in range(0, len(per), group):
+        ps = per[g0:g0 + group]
+        hs = [SketchHashes.draw(np.random.default_rng(p.seed), d, p.b) for p in ps]
+        stacked = SketchHashes(h1=sum((h.h1 for h in hs), ()), h2=sum((h.h2 for h in hs), ()),
+                               s1=sum((h.s1 for h in hs), ()), s2=sum((h.s2 for h in hs), ()))
+        words = stacked.packed_words()
+        D = d * len(ps)
+        if host:
+            acc = _device.compress_host(a_op, b_op, words, D, params.log2b, params.transform, _device.KMINOR, dev)
+        else:
+            acc = _device.compress_accumulate(a_op, b_op, words, D, params.log2b, params.transform, 0, n,
+                                              a_layout=_device.KMINOR, b_layout=_device.KMAJOR)
+        polys = _device.finalize(acc, D, params.log2b, params.transform)
+        for q, (p, h) in enumerate(zip(ps, hs)):
+            out.append(ProductSketch(polys=polys[q * d:(q + 1) * d].clone(), hashes=h, params=p, n_rows=n, n_cols=n))
+    return out
+
+
 # ----------------------------------------------------------------------------- decompress
 def combine_index(sketch: ProductSketch, k1: int, k2: int) -> int:
     """XOR for fwht, addition mod b for fft (sketch.py:343-347)."""

@@ -319,3 +319,26 @@ def test_extract_to_host_matches_device():
     assert torch.equal(host2, est_d[100:400].cpu())
     sel = (pairs_d[:, 0] >= 100) & (pairs_d[:, 0] < 400)
     assert torch.equal(pairs2, pairs_d[sel].cpu())
+
+
+@pytest.mark.parametrize("transform,log2b,d", [("fwht", 12, 5), ("fft", 11, 3), ("fwht", 10, 9)])
+def test_compress_seeds_equals_per_seed_compress(transform, log2b, d):
+    # Monte-Carlo batching: stacked repetitions, one launch per <= 63
+    rng = np.random.default_rng(5)
+    n = 384
+    a = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+    b = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+    p = P.SketchParams(n=n, b=1 << log2b, d=d, transform=transform, seed=0)
+    seeds = list(range(100, 100 + 15))  # 15 * 9 = 135 repetitions -> three launches for d = 9
+    many = P.compress_seeds(a, b, p, seeds)
+    for s, sk in zip(seeds, many):
+        one = P.compress(a, b, P.SketchParams(n=n, b=1 << log2b, d=d, transform=transform, seed=s))
+        assert sk.hashes == one.hashes and sk.params.seed == s
+        if transform == "fwht":
+            assert np.array_equal(sk.polys, one.polys)
+        else:
+            assert np.max(np.abs(sk.polys - one.polys)) <= 1e-12 * np.max(np.abs(one.polys))
+    # host operands take the streamed path
+    many_h = P.compress_seeds(a.cpu(), b.cpu(), p, seeds[:3])
+    for x, y in zip(many_h, many[:3]):
+        assert np.max(np.abs(x.polys - y.polys)) <= 1e-12 * np.max(np.abs(y.polys))

@@ -136,8 +136,14 @@ def test_abi_rejects_bad_parameters_before_any_kernel():
     words = np.zeros(8 * 3, dtype=np.uint64)
     wp = words.ctypes.data_as(ctypes.c_void_p)
     out = ctypes.c_int64(0)
-    # even depth, zero width, bad variant -> SMM_ERR_INVALID (maps to InvalidParameterError)
-    assert lib.smm_compress_workspace(1, 2, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
+    # depth out of range, zero width, bad variant -> SMM_ERR_INVALID (maps to InvalidParameterError);
+    # compress accepts even depths (stacked seeds, compress_seeds), extraction does not
+    assert lib.smm_compress_workspace(1, 0, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
+    assert lib.smm_compress_workspace(1, 64, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
+    assert lib.smm_compress_workspace(1, 2, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_OK
+    assert lib.smm_extract(1, None, wp, 2, 4, 8, 8, 0, 8, None, 8, 0.5, 1, None, 0, None, None, 0,
+                           None) == _lib.SMM_ERR_INVALID
+    assert b"odd" in lib.smm_last_error()
     assert lib.smm_compress_workspace(1, 3, 0, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
     assert lib.smm_compress_workspace(7, 3, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
     rc = lib.smm_compress_accumulate(1, None, 8, None, 8, 8, 8, 4, 2, wp, 3, 4, None, None, 0, None)
