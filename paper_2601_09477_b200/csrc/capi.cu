@@ -14,6 +14,11 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
                       int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws,
                       int64_t ws_bytes, cudaStream_t s);
 int add_inplace(double *dst, const double *src, int64_t n, cudaStream_t s);
+bool fft2p_supported(int log2b, int64_t n1, int64_t n2);
+int64_t fft2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K);
+int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb, int64_t n1,
+                     int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws, int64_t ws_bytes,
+                     cudaStream_t s);
 int fwht_accumulate(const SketchHashes &h, const double *at, int64_t ld_at, const double *bm, int64_t ld_bm,
                     int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc, char *ws, int64_t ws_bytes,
                     cudaStream_t s);
@@ -88,7 +93,7 @@ int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int
 // SMM_FLAG_ACCUMULATE: the two-pass kernel continues the k order in acc itself;
 // the other kernels reduce into a workspace accumulator that is then added.
 struct CompressPlan {
-  bool two_pass, acc_add;
+  bool two_pass, fft_two_pass, acc_add;
   bool ta, tb;  // transpose A / B slab
   int64_t ta_bytes, tb_bytes, tmp_acc_bytes, kernel_bytes;
 };
@@ -97,13 +102,15 @@ static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int
                                   int blay, bool acc_add) {
   CompressPlan c;
   c.acc_add = acc_add;
-  c.two_pass = variant == SMM_VARIANT_FWHT && fwht2p_supported(log2b, n1, n2);
+  c.fft_two_pass = variant == SMM_VARIANT_FFT && fft2p_supported(log2b, n1, n2);
+  c.two_pass = (variant == SMM_VARIANT_FWHT && fwht2p_supported(log2b, n1, n2)) || c.fft_two_pass;
   const int want = c.two_pass ? SMM_LAYOUT_KMINOR : SMM_LAYOUT_KMAJOR;
   c.ta = alay != want;
   c.tb = blay != want;
   c.ta_bytes = c.ta ? ((n1 * K * 8 + 255) / 256) * 256 : 0;
   c.tb_bytes = c.tb ? ((n2 * K * 8 + 255) / 256) * 256 : 0;
-  if (c.two_pass) c.kernel_bytes = fwht2p_workspace(d, log2b, n1, n2, K);
+  if (c.fft_two_pass) c.kernel_bytes = fft2p_workspace(d, log2b, n1, n2, K);
+  else if (c.two_pass) c.kernel_bytes = fwht2p_workspace(d, log2b, n1, n2, K);
   else if (variant == SMM_VARIANT_FWHT) c.kernel_bytes = fwht_workspace(d, log2b, n1, n2, K, num_sms());
   else c.kernel_bytes = fft_workspace(d, log2b, n1, n2, K, num_sms());
   c.tmp_acc_bytes = (acc_add && !c.two_pass) ? ((acc_bytes(variant, d, log2b) + 255) / 256) * 256 : 0;
@@ -185,6 +192,8 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
   }
   char *kws = ws + c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes;
   const int64_t kb = workspace_bytes - c.ta_bytes - c.tb_bytes - c.tmp_acc_bytes;
+  if (c.fft_two_pass)
+    return fft2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, acc_add, kws, kb, s);
   if (c.two_pass) return fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, acc_add, kws, kb, s);
   void *dst = acc_add ? (void *)(ws + c.ta_bytes + c.tb_bytes) : acc;
   if (variant == SMM_VARIANT_FWHT)

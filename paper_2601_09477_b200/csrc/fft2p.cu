@@ -1,0 +1,678 @@
+// FFT compress (steps 1-3, cyclic-convolution variant) for 2^8 <= b <= 2^14:
+// two-pass, persistent, dependency-ordered — the FFT counterpart of fwht2p.cu.
+// Reference: sketch.py:192-235 (`_compress_fft_kernel`), transforms.py:52-97.
+//
+// Per (repetition t, inner index k) the reference packs z = pa + i*pb, runs one
+// complex b-point FFT and accumulates FA(u)*FB(u), u in [0, b/2], with
+//   FA = (Z[u] + conj Z[-u]) / 2,   FB = -i/2 (Z[u] - conj Z[-u]).
+// Here the FFT is a four-step split b = 128 * N2 (m = m1 + 128 m2, u = u2 + N2 u1):
+//   pass 1 (gather item: 128 positions = 2^(7-S1) values of m1 x all m2):
+//     T[m1][u2] = w_b^(m1 u2) * DFT_N2 over m2 of z[m1 + 128 m2]     (S1 = log2 N2)
+//   pass 2 (slice item: one u2, or the pair {u2, N2-u2}):
+//     Z[u2 + N2 u1] = DFT_128 over m1 of T[m1][u2]
+// Both DFTs are radix-2 decimation in time with bit-reversed input, so the
+// gather scatters entry m straight to its bit-reversed position (the CSR key)
+// and every butterfly twiddle inside a pass depends only on the position inside
+// the 128-point tile (a 64-entry constant table).  Lanes carry 32 consecutive
+// inner indices k exactly as in fwht2p: each entry pulls one 256-byte row of the
+// k-minor operand; 16 complex values per thread (4 bits in registers), one
+// shared-memory exchange per pass (3 warp bits), T parked in L2 (3-slot ring).
+// Pass 2 transforms slice u2 (stashed in TMEM) and slice N2-u2 in the
+// "complement" layout, where a thread's register holding Z[u] for slice u2 holds
+// Z[-u] for the partner slice, so the FA/FB split is register-local; the two
+// self-paired slices (u2 = 0, N2/2) exchange partners through shared memory.
+// FA*FB is summed over the 32 lanes (k) in a fixed order and added to the
+// d x (b/2+1) accumulator in k-tile order (flags), so runs are bit-reproducible.
+#include <cmath>
+#include <cstdlib>
+
+#include "plan.cuh"
+#include "twopass.cuh"
+
+namespace smm {
+
+__global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b);  // fwht2p.cu
+__global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows);
+
+namespace f2p {
+using namespace tp;
+
+constexpr int THREADS = 256;
+constexpr int KT = 32;
+
+__constant__ double2 c_w128[64];  // exp(-2 pi i j / 128), j < 64
+
+// CSR key of bucket m: item * 128 + (m1 mod G) * N2 + rev_S1(m2)  (G = 128 / N2)
+__device__ __forceinline__ uint32_t fft_key(uint32_t m, int S1) {
+  const uint32_t m1 = m & 127u, m2 = m >> 7;
+  const uint32_t r2 = __brev(m2) >> (32 - S1);
+  const int gsh = 7 - S1;
+  return ((m1 >> gsh) << 7) | ((m1 & ((1u << gsh) - 1u)) << S1) | r2;
+}
+
+__global__ void csr_count_fft(SketchHashes h, int64_t n1, int64_t n2, int32_t *cnt, int64_t b, int S1) {
+  const int64_t per = n1 + n2;
+  const int64_t total = (int64_t)h.d * per;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x / per);
+    const int64_t q = x % per;
+    const int op = q < n1 ? 0 : 1;
+    const int64_t i = op ? q - n1 : q;
+    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b), S1);
+    atomicAdd(&cnt[((int64_t)t * 2 + op) * b + key], 1);
+  }
+}
+
+__global__ void csr_fill_fft(SketchHashes h, int64_t n1, int64_t n2, const int32_t *off, int32_t *fill, uint32_t *ent,
+                             int64_t nmax, int64_t b, int S1) {
+  const int64_t per = n1 + n2;
+  const int64_t total = (int64_t)h.d * per;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x / per);
+    const int64_t q = x % per;
+    const int op = q < n1 ? 0 : 1;
+    const int64_t i = op ? q - n1 : q;
+    const int64_t row = (int64_t)t * 2 + op;
+    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b), S1);
+    const uint32_t sb = eval_signbit(h.f[2 + op][t], (uint64_t)i);
+    const int32_t pos = off[row * (b + 1) + key] + atomicAdd(&fill[row * b + key], 1);
+    // entry: i (26 bits) | register (4 bits) | sign (1 bit)
+    ent[row * nmax + pos] = (uint32_t)i | ((key & 15u) << 26) | (sb << 31);
+  }
+}
+
+__global__ void twiddle_b_kernel(double *tw, int log2b) {
+  const int64_t b = (int64_t)1 << log2b;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < b; x += (int64_t)gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)x / (double)b, &s, &c);  // exact argument: x / b is a dyadic rational
+    tw[2 * x] = c;
+    tw[2 * x + 1] = s;
+  }
+}
+
+struct Args {
+  SketchHashes h;
+  const double *X[2];  // k-minor operands: element (i, k) at X[op][i * ld[op] + k]
+  int64_t ld[2];
+  int64_t k0, K;
+  int B, N2, G1, G2, U, d, lag, nslot;  // P2(u) is dispensed lag groups after P1(u); nslot = lag + 2
+  FastDiv div_d, div_slot, div_grp;
+  const int32_t *off;
+  const uint32_t *ent;
+  int64_t nmax, bsz;
+  const double *twb;  // [b][2]: exp(-2 pi i x / b)
+  double *Y;          // [nslot][N2][128][KT][2]
+  double *acc;        // [d][b/2 + 1][2]
+  int *ctr;           // [0] ticket | done1[U] | done2[U] | acc_cnt[d * G2]
+  int acc_add;
+};
+
+#define F2P_CASE(J)        \
+  case J:                  \
+    v[2 * J + OP] += val;  \
+    break;
+
+// signed gather of one operand into the real (op 0) or imaginary (op 1) parts;
+// warp w owns tile positions L in [16 w, 16 w + 16), register = L & 15
+template <int OP>
+__device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, double (&v)[32]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)t * 2 + OP;
+  const int32_t *off = p.off + row * (p.bsz + 1) + (int64_t)item * 128 + warp * 16;
+  const uint32_t *ent = p.ent + row * p.nmax;
+  const int e_lo = __ldg(off), e_hi = __ldg(off + 16);
+  const int64_t kk = (int64_t)kappa * KT + lane;
+  const char *Xb = (const char *)(p.X[OP] + p.k0 + (kk < p.K ? kk : p.K - 1));
+  const uint32_t ldb = (uint32_t)(p.ld[OP] * 8);
+  for (int eb = e_lo; eb < e_hi; eb += 8) {
+    const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
+    uint32_t es[8];
+    double x[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      x[s] = eb + s < e_hi ? __ldg((const double *)(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb)) : 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (eb + s < e_hi) {  // warp-uniform
+        const double val = (es[s] >> 31) ? -x[s] : x[s];
+        switch ((es[s] >> 26) & 15u) {
+          F2P_CASE(0) F2P_CASE(1) F2P_CASE(2) F2P_CASE(3) F2P_CASE(4) F2P_CASE(5) F2P_CASE(6) F2P_CASE(7)
+          F2P_CASE(8) F2P_CASE(9) F2P_CASE(10) F2P_CASE(11) F2P_CASE(12) F2P_CASE(13) F2P_CASE(14) F2P_CASE(15)
+          default: break;
+        }
+      }
+    }
+  }
+}
+
+// x' = x + y w, y' = x - y w
+__device__ __forceinline__ void bfly(double &xr, double &xi, double &yr, double &yi, double wr, double wi) {
+  const double tr = fma(yr, wr, -yi * wi);
+  const double ti = fma(yr, wi, yi * wr);
+  const double ar = xr, ai = xi;
+  xr = ar + tr;
+  xi = ai + ti;
+  yr = ar - tr;
+  yi = ai - ti;
+}
+__device__ __forceinline__ void bfly1(double &xr, double &xi, double &yr, double &yi) {
+  const double ar = xr, ai = xi;
+  xr = ar + yr;
+  xi = ai + yi;
+  yr = ar - yr;
+  yi = ai - yi;
+}
+
+// Radix-2 DIT stages s < NST (<= 4) over register bits (tile position L = (warp << 4) | r).
+// CMP: the thread's registers hold actual position 127 - L ("complement" layout).
+template <bool CMP, int NST>
+__device__ __forceinline__ void reg_stages(double (&v)[32]) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < NST) {
+      const int h = 1 << s;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (!(r & h)) {
+          const int j = CMP ? (h - 1 - (r & (h - 1))) : (r & (h - 1));
+          const int lo = CMP ? (r | h) : r, hi = CMP ? r : (r | h);  // lo: actual position bit s clear
+          if (j == 0) {
+            bfly1(v[2 * lo], v[2 * lo + 1], v[2 * hi], v[2 * hi + 1]);
+          } else {
+            const double2 w = c_w128[j << (6 - s)];
+            bfly(v[2 * lo], v[2 * lo + 1], v[2 * hi], v[2 * hi + 1], w.x, w.y);
+          }
+        }
+      }
+    }
+  }
+}
+
+// tile position of register r after the exchange: L bits 4-6 <- r bits 0-2, bit 3 <- r bit 3, bits 0-2 <- warp
+__device__ __forceinline__ int post_pos(int warp, int r) { return ((r & 7) << 4) | (r & 8) | warp; }
+
+// warp bits (L 4-6) <-> register bits 0-2 through shared memory (64 KB of complex values)
+__device__ __forceinline__ void exchange(double (&v)[32], double *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 *S2 = (double2 *)S;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S2[((warp << 4) | r) * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const double2 q = S2[post_pos(warp, r) * 32 + lane];
+    v[2 * r] = q.x;
+    v[2 * r + 1] = q.y;
+  }
+}
+
+// DIT stages 4 <= s < NST over register bits after the exchange
+template <bool CMP, int NST>
+__device__ __forceinline__ void post_stages(double (&v)[32]) {
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 4; s < 7; ++s) {
+    if (s < NST) {
+      const int bit = 1 << (s - 4), h = 1 << s;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (!(r & bit)) {
+          const int jn = post_pos(warp, r) & (h - 1);
+          const int j = CMP ? (h - 1 - jn) : jn;
+          const int lo = CMP ? (r | bit) : r, hi = CMP ? r : (r | bit);
+          const double2 w = c_w128[j << (6 - s)];
+          bfly(v[2 * lo], v[2 * lo + 1], v[2 * hi], v[2 * hi + 1], w.x, w.y);
+        }
+      }
+    }
+  }
+}
+
+// Pass 1: gather both operands of tile `item`, DFT_N2 over m2, twiddle w_b^(m1 u2), park T in L2
+template <int S1>
+__device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int slot, int item, double *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.0;
+  pull<0>(p, kappa, t, item, v);
+  pull<1>(p, kappa, t, item, v);
+  if ((int64_t)kappa * KT + KT > p.K && (int64_t)kappa * KT + lane >= p.K) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.0;
+  }
+  reg_stages<false, (S1 < 4 ? S1 : 4)>(v);
+  if (S1 > 4) {
+    exchange(v, S);
+    post_stages<false, S1>(v);
+  }
+  const uint64_t pol = policy_evict_last();
+  constexpr int G = 128 >> S1;  // values of m1 per tile
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int L = S1 > 4 ? post_pos(warp, r) : ((warp << 4) | r);
+    const int u2 = L & ((1 << S1) - 1);
+    const int m1 = item * G + (L >> S1);
+    const double2 w = __ldg((const double2 *)p.twb + m1 * u2);
+    const double re = fma(v[2 * r], w.x, -v[2 * r + 1] * w.y);
+    const double im = fma(v[2 * r], w.y, v[2 * r + 1] * w.x);
+    st2_hint(p.Y + ((((int64_t)slot * p.N2 + u2) * 128 + m1) * KT + lane) * 2, re, im, pol);
+  }
+}
+
+// full 128-point DIT DFT of slice u2 (T[., u2] in L2) into registers; CMP = complement layout
+template <bool CMP>
+__device__ __forceinline__ void slice_dft(const Args &p, int slot, int u2, double (&v)[32], double *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  const double *Ys = p.Y + (((int64_t)slot * p.N2 + u2) * 128) * KT * 2;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int pn = (warp << 4) | r;
+    const int pa = CMP ? 127 - pn : pn;
+    const int m1 = (int)(__brev((uint32_t)pa) >> 25);
+    ld2_hint(Ys + ((int64_t)m1 * KT + lane) * 2, v[2 * r], v[2 * r + 1], pol);
+  }
+  reg_stages<CMP, 4>(v);
+  exchange(v, S);  // its barrier also means every thread's loads of this slice completed
+  {
+    // last use of the slice's 64 KB: drop its L2 lines without write-back
+    const char *base = (const char *)Ys;
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (size_t)threadIdx.x * 256) : "memory");
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (size_t)threadIdx.x * 256 + 128) : "memory");
+  }
+  post_stages<CMP, 7>(v);
+  __syncthreads();  // shared memory is reused next
+}
+
+// FA * FB of Z[u] = (a, b) and Z[-u] = (c, e), in place of the second argument
+__device__ __forceinline__ void split_product(double a, double b, double &c, double &e) {
+  const double far = 0.5 * (a + c), fai = 0.5 * (b - e);   // FA = (Z[u] + conj Z[-u]) / 2
+  const double fbr = 0.5 * (b + e), fbi = -0.5 * (a - c);  // FB = -i/2 (Z[u] - conj Z[-u])
+  c = fma(far, fbr, -fai * fbi);
+  e = fma(far, fbi, fai * fbr);
+}
+
+// Pass 2: item i2 in [0, N2/2]: the slice pair {i2, N2 - i2}, or the self-paired 0 and N2/2
+__device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int slot, int i2, uint32_t tmem,
+                                        const int *acc_flag, double *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
+  const int N2 = p.N2;
+  const bool pair = i2 > 0 && 2 * i2 < N2;
+  // after the lane reduction this lane owns double `lane` = (register lane >> 1, re/im lane & 1)
+  const int u1 = post_pos(warp, lane >> 1);
+  int entry = -1;
+  bool conj = false;
+  if (pair) {
+    if (u1 < 64) entry = i2 + N2 * u1;
+    else { entry = (N2 - i2) + N2 * (127 - u1); conj = true; }
+  } else if (i2 == 0) {
+    if (u1 <= 64) entry = N2 * u1;
+  } else if (u1 <= 63) {
+    entry = i2 + N2 * u1;
+  }
+  double *a = entry >= 0 ? p.acc + (((int64_t)t * (p.bsz / 2 + 1) + entry) * 2 + (lane & 1)) : nullptr;
+  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
+  const double acc_old = (a && (kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
+  double v[32];
+  slice_dft<false>(p, slot, i2, v, S);
+  if (pair) {
+    const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st8(tq + 16 * c, v + 8 * c);
+    tmem_wait_st();
+    slice_dft<true>(p, slot, N2 - i2, v, S);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double zu[8];
+      tmem_ld8(tq + 16 * c, zu);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) split_product(zu[2 * q], zu[2 * q + 1], v[8 * c + 2 * q], v[8 * c + 2 * q + 1]);
+    }
+  } else {
+    // self-paired slice: Z[-u] sits at tile position -u1 (i2 = 0) or 127 - u1 (i2 = N2/2)
+    double2 *S2 = (double2 *)S;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) S2[post_pos(warp, r) * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int pu = post_pos(warp, r);
+      const int pm = i2 == 0 ? ((128 - pu) & 127) : (127 - pu);
+      const double2 zm = S2[pm * 32 + lane];
+      double c = zm.x, e = zm.y;
+      split_product(v[2 * r], v[2 * r + 1], c, e);
+      v[2 * r] = c;
+      v[2 * r + 1] = e;
+    }
+    __syncthreads();
+  }
+  // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory
+  double *W = S + warp * 1024;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) W[r * 32 + (lane ^ r)] = v[r];
+  __syncwarp();
+  double sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) sum += W[lane * 32 + (j ^ lane)];
+  if (conj && (lane & 1)) sum = -sum;  // entry b - u holds conj(FA FB (u))
+  if (a) {
+    if (kappa == 0) {
+      __stcg(a, p.acc_add ? acc_old + sum : sum);
+    } else if (acc_ready) {
+      __stcg(a, acc_old + sum);
+    }
+  }
+  if (kappa > 0 && !acc_ready) {
+    if (lane == 0)
+      while (flag < kappa) {
+        __nanosleep(32);
+        flag = ld_relaxed(acc_flag);
+      }
+    __syncwarp();
+    if (a) __stcg(a, __ldcg(a) + sum);
+  }
+}
+
+struct Item {
+  int64_t pos;
+  int is_p1, u, idx;
+};
+
+// order: [P1(0 .. lag-1) x G1] then groups g: [P1(g+lag) x G1][P2(g) x G2]; once g + lag >= U
+// the groups hold only [P2(g) x G2].  G1 = b / 128 is a power of two.
+__device__ __forceinline__ Item decode_item(const Args &p, int64_t pos) {
+  Item it;
+  it.pos = pos;
+  const int pro = p.U < p.lag ? p.U : p.lag;
+  const int lg1 = 31 - __clz(p.G1);
+  if (pos < (int64_t)pro * p.G1) {
+    it.is_p1 = 1; it.u = (int)(pos >> lg1); it.idx = (int)(pos & (p.G1 - 1));
+    return it;
+  }
+  const int q = (int)(pos - (int64_t)pro * p.G1);
+  const int full = p.U - pro;  // groups with a P1 part
+  const int regular = full * (p.G1 + p.G2);
+  if (q < regular) {
+    const int g = fdiv(q, p.div_grp);
+    const int r = q - g * (p.G1 + p.G2);
+    if (r < p.G1) { it.is_p1 = 1; it.u = g + p.lag; it.idx = r; }
+    else { it.is_p1 = 0; it.u = g; it.idx = r - p.G1; }
+  } else {
+    const int q2 = q - regular;
+    const int g2 = q2 / p.G2;
+    it.is_p1 = 0; it.u = full + g2; it.idx = q2 - g2 * p.G2;
+  }
+  return it;
+}
+
+template <int S1>
+__global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
+  extern __shared__ __align__(16) double S[];  // 64 KB: exchanges, partner lookups, lane reduction
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_item[8];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  int *ticket = p.ctr;
+  int *done1 = p.ctr + 1;
+  int *done2 = done1 + p.U;
+  int *acc_cnt = done2 + p.U;
+  const int64_t total = (int64_t)p.U * (p.G1 + p.G2);
+  // thread 0 schedules one item ahead (as fwht2p): the next ticket and the next
+  // item's dependency counter are fetched while the current item computes
+  int64_t nxt = 0;
+  Item itn;
+  const int *dep_ptr = nullptr;
+  int dep_target = 0, dep_val = 0;
+  int ver1 = -1, ver2 = -1;
+  auto probe = [&](const Item &it) {
+    dep_ptr = nullptr;
+    if (it.pos >= total) return;
+    if (it.is_p1) {
+      const int need = it.u - p.nslot;
+      if (need > ver2) { dep_ptr = done2 + need; dep_target = p.G2; }
+    } else if (it.u > ver1) {
+      dep_ptr = done1 + it.u;
+      dep_target = p.G1;
+    }
+    if (dep_ptr) dep_val = ld_acquire(dep_ptr);
+  };
+  if (tid == 0) {
+    const int64_t cur = atomicAdd(ticket, 1);
+    nxt = atomicAdd(ticket, 1);
+    itn = decode_item(p, cur);
+    probe(itn);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  while (true) {
+    if (tid == 0) {
+      const Item it = itn;
+      if (dep_ptr) {  // dispensed earlier than this item: cannot deadlock
+        while (dep_val < dep_target) {
+          __nanosleep(64);
+          dep_val = ld_acquire(dep_ptr);
+        }
+        if (it.is_p1) ver2 = it.u - p.nslot;
+        else ver1 = it.u;
+      }
+      s_item[0] = it.pos < total ? 1 : 0;
+      s_item[1] = it.is_p1;
+      s_item[2] = it.u;
+      s_item[3] = it.idx;
+      s_item[4] = fdiv(it.u, p.div_d);             // kappa
+      s_item[5] = fmod_(it.u, p.div_d);            // t
+      s_item[6] = fmod_(it.u, p.div_slot);         // Y slot
+      itn = decode_item(p, nxt);
+    }
+    tc_fence_before();
+    __syncthreads();  // [A]
+    tc_fence_after();
+    const int go = s_item[0];
+    const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
+    const int kappa = s_item[4], t = s_item[5], slot = s_item[6];
+    if (tid == 0 && go) {
+      probe(itn);
+      nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
+    }
+    if (!go) break;
+    if (is_p1) p1_item<S1>(p, kappa, t, slot, idx, S);
+    else p2_item(p, kappa, t, slot, idx, tmem, acc_cnt + t * p.G2 + idx, S);
+    tc_fence_before();
+    __syncthreads();  // [B]
+    tc_fence_after();
+    if (tid == 32) {  // publish (release covers the CTA's writes through [B])
+      fence_acq_rel();
+      if (is_p1) red_add(done1 + u, 1);
+      else {
+        red_add(acc_cnt + t * p.G2 + idx, 1);
+        red_add(done2 + u, 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
+
+static int init_w128(cudaStream_t s) {
+  static bool done[64] = {false};
+  int dev = 0;
+  SMM_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 64 && done[dev]) return SMM_OK;
+  double2 w[64];
+  for (int j = 0; j < 64; ++j) {
+    const double ang = M_PI * (double)j / 64.0;  // 2 pi j / 128
+    w[j] = make_double2(std::cos(ang), -std::sin(ang));
+  }
+  SMM_CUDA_TRY(cudaMemcpyToSymbolAsync(c_w128, w, sizeof(w), 0, cudaMemcpyHostToDevice, s), "w128 table");
+  SMM_CUDA_TRY(cudaStreamSynchronize(s), "w128 table");
+  if (dev < 64) done[dev] = true;
+  return SMM_OK;
+}
+
+}  // namespace f2p
+
+bool fft2p_supported(int log2b, int64_t n1, int64_t n2) {
+  return log2b >= 8 && log2b <= 14 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
+}
+
+namespace f2p {
+// units in flight: ~2 CTAs per SM need about 2 * num_sms items; a group dispenses G1 + G2
+static int lag_for(int log2b) {
+  const int b7 = 1 << (log2b - 7);
+  int lag = 2 * num_sms() / (b7 + b7 / 2 + 1);
+  return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+}
+}  // namespace f2p
+
+int64_t fft2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
+  using f2p::pad256;
+  const int64_t b = (int64_t)1 << log2b;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  const int64_t ntiles = (K + f2p::KT - 1) / f2p::KT;
+  const int64_t U = ntiles * d;
+  const int64_t N2 = b >> 7;
+  const int64_t G2 = N2 / 2 + 1;
+  int64_t w = 0;
+  w += pad256((int64_t)d * 2 * (b + 1) * 4);                 // off
+  w += pad256((int64_t)d * 2 * b * 4);                       // cnt / fill
+  w += pad256((int64_t)d * 2 * nmax * 4);                    // ent
+  w += pad256(b * 16);                                       // twiddles w_b^x
+  w += pad256((int64_t)(f2p::lag_for(log2b) + 2) * b * f2p::KT * 16);  // T ring
+  w += pad256((1 + 2 * U + (int64_t)d * G2) * 4);            // counters
+  return w;
+}
+
+int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb, int64_t n1,
+                     int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws, int64_t ws_bytes,
+                     cudaStream_t s) {
+  using namespace f2p;
+  const int d = h.d, log2b = h.log2b;
+  const int64_t b = (int64_t)1 << log2b;
+  const int64_t K = k1 - k0;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  const int S1 = log2b - 7;
+  if (lda >= ((int64_t)1 << 28) || ldb >= ((int64_t)1 << 28)) {
+    set_error("operand row stride too large for the two-pass kernel");
+    return SMM_ERR_INVALID;
+  }
+  if (ws_bytes < fft2p_workspace(d, log2b, n1, n2, K)) {
+    set_error("compress workspace too small (two-pass fft)");
+    return SMM_ERR_WORKSPACE;
+  }
+  char *q = ws;
+  int32_t *off = (int32_t *)q;
+  q += pad256((int64_t)d * 2 * (b + 1) * 4);
+  int32_t *cnt = (int32_t *)q;
+  q += pad256((int64_t)d * 2 * b * 4);
+  uint32_t *ent = (uint32_t *)q;
+  q += pad256((int64_t)d * 2 * nmax * 4);
+  double *twb = (double *)q;
+  q += pad256(b * 16);
+  double *Y = (double *)q;
+  const int lag = lag_for(log2b);
+  const int nslot = lag + 2;
+  q += pad256((int64_t)nslot * b * KT * 16);
+  int *ctr = (int *)q;
+  const int64_t ntiles = (K + KT - 1) / KT;
+  const int64_t U = ntiles * d;
+  const int N2 = (int)(b >> 7);
+  const int G1 = (int)(b >> 7);  // 128-position gather tiles per unit
+  const int G2 = N2 / 2 + 1;     // slice pairs + the two self-paired slices
+  const size_t acc_bytes = (size_t)d * (size_t)(b / 2 + 1) * 16;
+  if (K <= 0) {
+    if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, acc_bytes, s), "acc memset");
+    return SMM_OK;
+  }
+  if (U * (G1 + G2) > ((int64_t)1 << 30)) {
+    set_error("inner range too large for one call");
+    return SMM_ERR_INVALID;
+  }
+  int rc = init_w128(s);
+  if (rc) return rc;
+  twiddle_b_kernel<<<(unsigned)ceil_div(b, 256) > 1024 ? 1024 : (unsigned)ceil_div(b, 256), 256, 0, s>>>(twb, log2b);
+  SMM_LAUNCH_CHECK("twiddle_b_kernel");
+  // plan: CSR by bit-reversed tile position
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  const int64_t nin = (int64_t)d * (n1 + n2);
+  int64_t blocks = ceil_div(nin, 256);
+  if (blocks > 8192) blocks = 8192;
+  if (nin > 0) {
+    csr_count_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, b, S1);
+    SMM_LAUNCH_CHECK("csr_count_fft");
+  }
+  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, b);
+  SMM_LAUNCH_CHECK("csr_scan_kernel");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  if (nin > 0) {
+    csr_fill_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, b, S1);
+    SMM_LAUNCH_CHECK("csr_fill_fft");
+    int64_t sb = ceil_div((int64_t)d * 2 * b, 256);
+    if (sb > 8192) sb = 8192;
+    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, b, d * 2);
+    SMM_LAUNCH_CHECK("csr_sort_kernel");
+  }
+  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * G2) * 4, s), "counter memset");
+  Args p;
+  p.h = h;
+  p.X[0] = xa;
+  p.X[1] = xb;
+  p.ld[0] = lda;
+  p.ld[1] = ldb;
+  p.k0 = k0;
+  p.K = K;
+  p.B = log2b;
+  p.N2 = N2;
+  p.G1 = G1;
+  p.G2 = G2;
+  p.U = (int)U;
+  p.d = d;
+  p.div_d = make_fastdiv((uint32_t)d);
+  p.div_slot = make_fastdiv((uint32_t)nslot);
+  p.lag = lag;
+  p.nslot = nslot;
+  p.div_grp = make_fastdiv((uint32_t)(G1 + G2));
+  p.off = off;
+  p.ent = ent;
+  p.nmax = nmax;
+  p.bsz = b;
+  p.twb = twb;
+  p.Y = Y;
+  p.acc = acc;
+  p.ctr = ctr;
+  p.acc_add = acc_add ? 1 : 0;
+  const size_t smem = (size_t)8 * 32 * 32 * 8;
+  const int G = 2 * num_sms();
+  switch (S1) {
+#define F2P_LAUNCH(SS)                                                                                 \
+  case SS:                                                                                            \
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fft2p_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+                 "fft2p smem");                                                                       \
+    fft2p_kernel<SS><<<G, THREADS, smem, s>>>(p);                                                     \
+    break;
+    F2P_LAUNCH(1) F2P_LAUNCH(2) F2P_LAUNCH(3) F2P_LAUNCH(4) F2P_LAUNCH(5) F2P_LAUNCH(6) F2P_LAUNCH(7)
+#undef F2P_LAUNCH
+    default:
+      set_error("two-pass fft kernel: unsupported width");
+      return SMM_ERR_INVALID;
+  }
+  SMM_LAUNCH_CHECK("fft2p_kernel");
+  return SMM_OK;
+}
+
+}  // namespace smm

@@ -33,7 +33,8 @@ namespace smm {
 constexpr int P_THREADS = 256;
 constexpr int KT = 32;
 constexpr int P1_BITS = 8;
-#define SMM_LAG 1  // P2(u) is dispensed LAG groups after P1(u) (2 was measured slower on cfg3)
+// P2(u) is dispensed `lag` groups after P1(u) (lag_for(): 1 at b = 2^16, where 2 was
+// measured slower; small transforms have few items per unit and need more units in flight)
 
 // Optional phase profiler (env SMM_PROFILE=1): thread 0 of every CTA accumulates
 // clock64 deltas between marks; printed by the host after the launch.
@@ -164,6 +165,7 @@ struct TwoPassArgs {
   int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
   long long *prof;  // [16] phase cycles (nullable)
   int acc_add;      // add to acc (continue an earlier call's k order) instead of overwriting it
+  int lag;          // pipeline depth in units (nslot = lag + 2)
 };
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -461,7 +463,7 @@ __device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, i
   // prologue: P1 of units 0..LAG-1; then groups g = 0..U-1: [P1(g+LAG) x nblk][P2(g) x nblk]
   // (the P1 part is absent once g+LAG >= U).  2*nblk is a power of two.
   const int G1 = p.nblk;  // = 2^(log2g - 1)
-  const int pro_units = p.U < SMM_LAG ? p.U : SMM_LAG;
+  const int pro_units = p.U < p.lag ? p.U : p.lag;
   Item it;
   it.pos = pos;
   if (pos < (int64_t)pro_units * G1) {
@@ -469,12 +471,12 @@ __device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, i
     return it;
   }
   const int q = (int)(pos - (int64_t)pro_units * G1);
-  const int full = p.U > SMM_LAG ? p.U - SMM_LAG : 0;
+  const int full = p.U > p.lag ? p.U - p.lag : 0;
   const int regular = full << log2g;
   if (q < regular) {
     const int g = q >> log2g;
     const int r = q & ((1 << log2g) - 1);
-    if (r < G1) { it.is_p1 = 1; it.u = g + SMM_LAG; it.idx = r; }
+    if (r < G1) { it.is_p1 = 1; it.u = g + p.lag; it.idx = r; }
     else { it.is_p1 = 0; it.u = g; it.idx = r - G1; }
   } else {
     const int q2 = q - regular;
@@ -621,11 +623,21 @@ static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
 constexpr int MAX_LB = 16;  // per-slice transform bits handled by the two passes (8 + 8)
 
+// Chosen when it is the faster kernel: with more inputs than buckets (b < n) the
+// gather dominates and the fold kernels' row-streaming scatter wins (cfg5 b=2^12,
+// n=8192: 4.2 ms vs 7.3 ms); from b = 2^16 on the two-pass kernel always wins.
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
-  return log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  const bool faster = log2b >= 16 || ((int64_t)1 << log2b) >= nmax;
+  return faster && log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
-static int nslots_for(int) { return 3; }
+// units in flight: ~2 CTAs per SM need about 2 * num_sms items; a unit dispenses 2 * nblk
+static int lag_for(int LB) {
+  const int nblk = 1 << (LB - P1_BITS);
+  int lag = num_sms() / nblk;
+  return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+}
 
 // geometry: LB-bit slices, F = 2^(log2b - LB) of them (the fold of DESIGN.md §5)
 static void fwht2p_geometry(int log2b, int &LB, int &F) {
@@ -645,7 +657,7 @@ int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   w += pad256((int64_t)d * 2 * (bs + 1) * 4);  // off
   w += pad256((int64_t)d * 2 * bs * 4);        // cnt / fill
   w += pad256((int64_t)d * 2 * nmax * 4);      // ent
-  w += pad256((int64_t)nslots_for(log2b) * 2 * bs * KT * 8);  // Y ring
+  w += pad256((int64_t)(lag_for(LB) + 2) * 2 * bs * KT * 8);  // Y ring
   w += pad256((1 + 2 * U + (int64_t)d * F * nblk) * 4);       // counters
   return w;
 }
@@ -676,7 +688,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   uint32_t *ent = (uint32_t *)q;
   q += pad256((int64_t)d * 2 * nmax * 4);
   double *Y = (double *)q;
-  const int nslot = nslots_for(log2b);
+  const int lag = lag_for(LB);
+  const int nslot = lag + 2;
   q += pad256((int64_t)nslot * 2 * bs * KT * 8);
   int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;
@@ -741,6 +754,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.ctr = ctr;
   p.prof = nullptr;
   p.acc_add = acc_add ? 1 : 0;
+  p.lag = lag;
   static const bool prof_on = getenv("SMM_PROFILE") != nullptr;
   if (prof_on) {
     cudaMalloc((void **)&p.prof, 16 * sizeof(long long));
