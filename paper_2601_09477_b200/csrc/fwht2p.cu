@@ -294,9 +294,14 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
   const uint32_t *ent = p.ent + row * p.nmax;
   const int e_lo = hd.e_lo;
   const int e_hi = hd.e_hi;
-  double v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = 0.0;
+  // Scatter into this lane's column of the warp's rows of the exchange area
+  // (S[(warp * 32 + j) * 32 + lane], lane-private: no barrier), not into registers:
+  // a register target needs a data-dependent jump per entry, which measured ~7 ms
+  // of instruction-fetch stalls on cfg3.  Entries are sorted by bucket, so the
+  // first entry of a bucket stores and later ones add (CSR order, as before).
+  double *col = S + warp * 1024 + lane;
+  uint32_t mask = 0;  // buckets with an entry (warp-uniform)
+  int prevj = -1;
   for (int eb = e_lo; eb < e_hi; eb += 8) {
     const uint32_t mine =
         eb == e_lo ? hd.first : ((lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u);
@@ -317,16 +322,16 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
         if (p.F > 1)  // fold character of slice a: (-1)^popcount(a & (h(i) >> LB))
           neg ^= __popc((eval_bucket(p.h.f[op][t], (uint64_t)(es[s] & 0x03ffffffu), p.B) >> p.LB) & (uint32_t)a) & 1u;
         const double val = neg ? -x[s] : x[s];
-        switch (j) {
-          SMM_CASE(0) SMM_CASE(1) SMM_CASE(2) SMM_CASE(3) SMM_CASE(4) SMM_CASE(5) SMM_CASE(6) SMM_CASE(7)
-          SMM_CASE(8) SMM_CASE(9) SMM_CASE(10) SMM_CASE(11) SMM_CASE(12) SMM_CASE(13) SMM_CASE(14) SMM_CASE(15)
-          SMM_CASE(16) SMM_CASE(17) SMM_CASE(18) SMM_CASE(19) SMM_CASE(20) SMM_CASE(21) SMM_CASE(22) SMM_CASE(23)
-          SMM_CASE(24) SMM_CASE(25) SMM_CASE(26) SMM_CASE(27) SMM_CASE(28) SMM_CASE(29) SMM_CASE(30) SMM_CASE(31)
-          default: break;
-        }
+        const double old = j == prevj ? col[j * 32] : 0.0;  // 0 + val == val, as the register path
+        col[j * 32] = old + val;
+        mask |= 1u << j;
+        prevj = j;
       }
     }
   }
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = ((mask >> j) & 1u) ? col[j * 32] : 0.0;
   if (!full_tile && kk >= p.K) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = 0.0;
