@@ -533,9 +533,14 @@ bool fft2p_supported(int log2b, int64_t n1, int64_t n2) {
 
 namespace f2p {
 // units in flight: ~2 CTAs per SM need about 2 * num_sms items; a group dispenses G1 + G2
+// units in flight: about 4 items per SM (2 CTAs x 2) must be dispensable, and a
+// group dispenses G1 + G2; the T ring ((lag + 2) slots of b x 32 complex) stays within ~64 MB
 static int lag_for(int log2b) {
   const int b7 = 1 << (log2b - 7);
-  int lag = 2 * num_sms() / (b7 + b7 / 2 + 1);
+  const int grp = b7 + b7 / 2 + 1;
+  int lag = (4 * num_sms() + grp - 1) / grp;
+  const int cap = (int)(((int64_t)64 << 20) / (((int64_t)1 << log2b) * KT * 16)) - 2;
+  if (lag > cap) lag = cap;
   return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
 }
 }  // namespace f2p

@@ -638,9 +638,14 @@ bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
 }
 
 // units in flight: ~2 CTAs per SM need about 2 * num_sms items; a unit dispenses 2 * nblk
+// units in flight: about 4 items per SM (2 CTAs x 2) must be dispensable, and a
+// group dispenses 2 * nblk; the Y ring ((lag + 2) slots) stays within ~64 MB of L2
 static int lag_for(int LB) {
   const int nblk = 1 << (LB - P1_BITS);
-  int lag = num_sms() / nblk;
+  const int64_t slot = (int64_t)2 * (1 << LB) * KT * 8;
+  int lag = (4 * num_sms() + 2 * nblk - 1) / (2 * nblk);
+  const int cap = (int)(((int64_t)64 << 20) / slot) - 2;
+  if (lag > cap) lag = cap;
   return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
 }
 
