@@ -16,7 +16,7 @@
 // the 128-point tile (a 64-entry constant table).  Lanes carry 32 consecutive
 // inner indices k exactly as in fwht2p: each entry pulls one 256-byte row of the
 // k-minor operand; 16 complex values per thread (4 bits in registers), one
-// shared-memory exchange per pass (3 warp bits), T parked in L2 (3-slot ring).
+// shared-memory exchange per pass (3 warp bits), T parked in L2 ((lag+2)-slot ring).
 // Pass 2 transforms slice u2 (stashed in TMEM) and slice N2-u2 in the
 // "complement" layout, where a thread's register holding Z[u] for slice u2 holds
 // Z[-u] for the partner slice, so the FA/FB split is register-local; the two

@@ -1,4 +1,4 @@
-// FWHT compress v2 (steps 1-3) for 2^9 <= b <= 2^16: two-pass, persistent,
+// FWHT compress (steps 1-3) for 2^8 <= b <= 2^20: two-pass, persistent,
 // dependency-ordered.  Reference: sketch.py:152-189, transforms.py:37-49.
 //
 // Why two passes.  A length-b FP64 transform does log2(b) adds per element;
@@ -7,23 +7,23 @@
 // stages and a random-access scatter costs ~3x more.  This kernel therefore
 // (1) makes the scatter a *coalesced* pull: lanes carry 32 consecutive inner
 // indices k, so each input element i contributes one 256-byte row segment
-// X[i, k0:k0+32] of the k-minor operand (A row-major, B^T row-major); (2)
-// keeps bucket bits in registers (5 stages free), moves 4 more bits through
-// ONE shared-memory exchange (pass 1, 9 low bits) and up to 2 more through a
-// tensor-memory (TMEM) exchange (pass 2, high bits) — TMEM ld/st run at
-// 177/400 B/clk/SM on a datapath separate from shared memory; (3) parks the
-// pass-1 result Y (b x 32 doubles per repetition and operand) in the 126 MB
-// L2 between the passes, in a 3-slot ring; (4) accumulates FA*FB over k in
-// registers (lane reduction) and adds it to the d x b accumulator once per
-// k-tile.
+// X[i, k0:k0+32] of the k-minor operand (A row-major, B^T row-major), scattered
+// into the warp's lane-private columns of the exchange area; (2) keeps 5 bucket
+// bits in registers (free stages) and moves 3 more through ONE shared-memory
+// exchange per pass (pass 1: 8 low bits, pass 2: up to 8 high bits); (3) parks
+// the pass-1 result Y (2^LB x 32 doubles per repetition and operand) in the
+// 126 MB L2 between the passes, in a (lag + 2)-slot ring; (4) keeps the first
+// operand's pass-2 result in TMEM until the product, sums FA*FB over the 32
+// lanes and adds it to the d x b accumulator once per k-tile.  b > 2^16 is
+// folded into F = b / 2^16 slices (one sign per entry).
 //
-// Scheduling: one persistent CTA per SM pulls tickets from a global counter in
-// a fixed order [P1(0)] [P1(1) P2(0)] [P1(2) P2(1)] ... where a unit u is
-// (k-tile kappa = u / d, repetition t = u % d).  Every item's dependencies
-// (P2(u) needs all P1(u); P1(u) reuses the Y slot of P2(u-3); P2(kappa, t, s)
-// extends the accumulator after P2(kappa-1, t, s)) are dispensed earlier, so
-// spinning on them cannot deadlock; accumulator updates happen in k order, so
-// results are bit-reproducible.
+// Scheduling: two persistent CTAs per SM pull tickets from a global counter in
+// a fixed order [P1(0..lag-1)] [P1(lag) P2(0)] [P1(lag+1) P2(1)] ... where a
+// unit u is (k-tile kappa, repetition t, fold slice a).  Every item's
+// dependencies (P2(u) needs all P1(u); P1(u) reuses the Y slot of
+// P2(u - nslot); P2(kappa, t, s) extends the accumulator after P2(kappa-1, t, s))
+// are dispensed earlier, so spinning on them cannot deadlock; accumulator
+// updates happen in k order, so results are bit-reproducible.
 #include <cstdlib>
 
 #include "plan.cuh"
