@@ -18,7 +18,7 @@
 namespace smm {
 
 constexpr int XT = 256;
-constexpr int XROWS = 16;
+constexpr int XROWS = 64;
 
 template <int D>
 __device__ __forceinline__ double median_sorted(double (&v)[D]) {
@@ -52,6 +52,9 @@ template <int D>
 __global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
   const int d = D > 0 ? D : p.h.d;
   constexpr int DM = D > 0 ? D : SMM_MAX_DEPTH;
+  // rows per group whose gathers are in flight together (latency of the random
+  // L2 gathers is the bound: d * RG independent 8-byte loads per thread)
+  constexpr int RG = D > 0 ? 4 : 1;
   __shared__ uint32_t s_h1[XROWS][DM];
   __shared__ int8_t s_s1[XROWS][DM];
   const int log2b = p.h.log2b;
@@ -77,39 +80,52 @@ __global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
     }
   }
   const int lane = threadIdx.x & 31;
-  for (int r = 0; r < nrows; ++r) {
-    const int64_t i = rbase + r;
-    double v[DM];
+  for (int r0 = 0; r0 < nrows; r0 += RG) {
+    double v[RG][DM];
 #pragma unroll
-    for (int t = 0; t < DM; ++t) {
-      if (t < d) {
-        const uint32_t a = s_h1[r][t];
-        const uint32_t idx = p.xor_combine ? (a ^ h2[t]) : ((a + h2[t]) & bmask);
-        double x = colok ? __ldg(p.polys + t * b + idx) : 0.0;
-        x *= (double)s_s1[r][t];  // vals *= s1 ; vals *= s2 (sketch.py:396-397)
-        x *= s2[t];
-        v[t] = x;
+    for (int g = 0; g < RG; ++g) {
+      const int r = r0 + g < nrows ? r0 + g : nrows - 1;  // clamped duplicate rows are not stored
+#pragma unroll
+      for (int t = 0; t < DM; ++t) {
+        if (t < d) {
+          const uint32_t a = s_h1[r][t];
+          const uint32_t idx = p.xor_combine ? (a ^ h2[t]) : ((a + h2[t]) & bmask);
+          v[g][t] = colok ? __ldg(p.polys + t * b + idx) : 0.0;
+        }
       }
     }
-    double e;
-    if (D > 0) {
-      e = median_sorted<DM>(v);
-    } else {
-      for (int a = 1; a < d; ++a) {
-        double key = v[a];
-        int q = a - 1;
-        while (q >= 0 && v[q] > key) { v[q + 1] = v[q]; --q; }
-        v[q + 1] = key;
+#pragma unroll
+    for (int g = 0; g < RG; ++g) {
+      const int r = r0 + g;
+      if (r >= nrows) break;  // block-uniform
+      const int64_t i = rbase + r;
+#pragma unroll
+      for (int t = 0; t < DM; ++t) {
+        if (t < d) {
+          v[g][t] *= (double)s_s1[r][t];  // vals *= s1 ; vals *= s2 (sketch.py:396-397)
+          v[g][t] *= s2[t];
+        }
       }
-      e = v[(d - 1) / 2];
-    }
-    if (colok && p.est) p.est[(i - p.r0) * p.ld_est + j] = e;
-    const double ae = fabs(e);
-    const bool hit = colok && (p.strict ? (ae > p.thr) : (ae >= p.thr));
-    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0 && (j >> 5) < p.mask_ld) {
-      p.mask[(i - p.r0) * p.mask_ld + (j >> 5)] = bal;
-      if (bal) atomicAdd((unsigned long long *)&p.rowcnt[i - p.r0], (unsigned long long)__popc(bal));
+      double e;
+      if (D > 0) {
+        e = median_sorted<DM>(v[g]);
+      } else {
+        for (int a = 1; a < d; ++a) {
+          double key = v[g][a];
+          int q = a - 1;
+          while (q >= 0 && v[g][q] > key) { v[g][q + 1] = v[g][q]; --q; }
+          v[g][q + 1] = key;
+        }
+        e = v[g][(d - 1) / 2];
+      }
+      if (colok && p.est) p.est[(i - p.r0) * p.ld_est + j] = e;
+      const double ae = fabs(e);
+      const bool hit = colok && (p.strict ? (ae > p.thr) : (ae >= p.thr));
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0 && (j >> 5) < p.mask_ld) {
+        p.mask[(i - p.r0) * p.mask_ld + (j >> 5)] = bal;
+        if (bal) atomicAdd((unsigned long long *)&p.rowcnt[i - p.r0], (unsigned long long)__popc(bal));
+      }
     }
   }
 }
