@@ -108,15 +108,13 @@ struct Args {
   int acc_add;
 };
 
-#define F2P_CASE(J)        \
-  case J:                  \
-    v[2 * J + OP] += val;  \
-    break;
-
-// signed gather of one operand into the real (op 0) or imaginary (op 1) parts;
-// warp w owns tile positions L in [16 w, 16 w + 16), register = L & 15
+// signed gather of one operand into the real (op 0) or imaginary (op 1) parts of the
+// warp's lane-private complex columns of the exchange area (S2[(16 w + j) * 32 + lane],
+// j = tile position & 15) — a register target would need a jump per entry.  Entries
+// are sorted by position: the first of a position stores, later ones add.  Returns the
+// mask of positions written.
 template <int OP>
-__device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, double (&v)[32]) {
+__device__ __forceinline__ uint32_t pull(const Args &p, int kappa, int t, int item, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)t * 2 + OP;
   const int32_t *off = p.off + row * (p.bsz + 1) + (int64_t)item * 128 + warp * 16;
@@ -125,6 +123,9 @@ __device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, 
   const int64_t kk = (int64_t)kappa * KT + lane;
   const char *Xb = (const char *)(p.X[OP] + p.k0 + (kk < p.K ? kk : p.K - 1));
   const uint32_t ldb = (uint32_t)(p.ld[OP] * 8);
+  double *col = S + ((warp * 16) * 32 + lane) * 2 + OP;
+  uint32_t mask = 0;
+  int prevj = -1;
   for (int eb = e_lo; eb < e_hi; eb += 8) {
     const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
     uint32_t es[8];
@@ -137,15 +138,16 @@ __device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, 
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       if (eb + s < e_hi) {  // warp-uniform
+        const int j = (int)((es[s] >> 26) & 15u);
         const double val = (es[s] >> 31) ? -x[s] : x[s];
-        switch ((es[s] >> 26) & 15u) {
-          F2P_CASE(0) F2P_CASE(1) F2P_CASE(2) F2P_CASE(3) F2P_CASE(4) F2P_CASE(5) F2P_CASE(6) F2P_CASE(7)
-          F2P_CASE(8) F2P_CASE(9) F2P_CASE(10) F2P_CASE(11) F2P_CASE(12) F2P_CASE(13) F2P_CASE(14) F2P_CASE(15)
-          default: break;
-        }
+        const double old = j == prevj ? col[j * 64] : 0.0;  // 0 + val == val, as a register sum
+        col[j * 64] = old + val;
+        mask |= 1u << j;
+        prevj = j;
       }
     }
   }
+  return mask;
 }
 
 // x' = x + y w, y' = x - y w
@@ -235,11 +237,17 @@ __device__ __forceinline__ void post_stages(double (&v)[32]) {
 template <int S1>
 __device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int slot, int item, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m0 = pull<0>(p, kappa, t, item, S);
+  const uint32_t m1 = pull<1>(p, kappa, t, item, S);
   double v[32];
+  {
+    const double *col = S + ((warp * 16) * 32 + lane) * 2;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = 0.0;
-  pull<0>(p, kappa, t, item, v);
-  pull<1>(p, kappa, t, item, v);
+    for (int j = 0; j < 16; ++j) {
+      v[2 * j] = ((m0 >> j) & 1u) ? col[j * 64] : 0.0;
+      v[2 * j + 1] = ((m1 >> j) & 1u) ? col[j * 64 + 1] : 0.0;
+    }
+  }
   if ((int64_t)kappa * KT + KT > p.K && (int64_t)kappa * KT + lane >= p.K) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = 0.0;
