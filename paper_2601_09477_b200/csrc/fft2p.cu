@@ -50,6 +50,7 @@ __device__ __forceinline__ uint32_t fft_key(uint32_t m, int S1) {
   return ((m1 >> gsh) << 7) | ((m1 & ((1u << gsh) - 1u)) << S1) | r2;
 }
 
+// b here is the slice size 2^LBs: a bucket's key is its position within the slice
 __global__ void csr_count_fft(SketchHashes h, int64_t n1, int64_t n2, int32_t *cnt, int64_t b, int S1) {
   const int64_t per = n1 + n2;
   const int64_t total = (int64_t)h.d * per;
@@ -58,7 +59,7 @@ __global__ void csr_count_fft(SketchHashes h, int64_t n1, int64_t n2, int32_t *c
     const int64_t q = x % per;
     const int op = q < n1 ? 0 : 1;
     const int64_t i = op ? q - n1 : q;
-    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b), S1);
+    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b) & (uint32_t)(b - 1), S1);
     atomicAdd(&cnt[((int64_t)t * 2 + op) * b + key], 1);
   }
 }
@@ -73,7 +74,7 @@ __global__ void csr_fill_fft(SketchHashes h, int64_t n1, int64_t n2, const int32
     const int op = q < n1 ? 0 : 1;
     const int64_t i = op ? q - n1 : q;
     const int64_t row = (int64_t)t * 2 + op;
-    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b), S1);
+    const uint32_t key = fft_key(eval_bucket(h.f[op][t], (uint64_t)i, h.log2b) & (uint32_t)(b - 1), S1);
     const uint32_t sb = eval_signbit(h.f[2 + op][t], (uint64_t)i);
     const int32_t pos = off[row * (b + 1) + key] + atomicAdd(&fill[row * b + key], 1);
     // entry: i (26 bits) | register (4 bits) | sign (1 bit)
@@ -97,14 +98,15 @@ struct Args {
   int64_t ld[2];
   int64_t k0, K;
   int B, N2, G1, G2, U, d, lag, nslot;  // P2(u) is dispensed lag groups after P1(u); nslot = lag + 2
-  FastDiv div_d, div_slot, div_grp;
+  int F, NPU, halves;  // fold: F slices of 2^LBs frequencies; NPU slice-pair units per (k-tile, t)
+  FastDiv div_dnpu, div_npu, div_slot, div_grp;
   const int32_t *off;
   const uint32_t *ent;
-  int64_t nmax, bsz;
+  int64_t nmax, bsz, bfull;  // bsz = slice size 2^LBs (CSR rows), bfull = b
   const double *twb;  // [b][2]: exp(-2 pi i x / b)
-  double *Y;          // [nslot][N2][128][KT][2]
+  double *Y;          // [nslot][halves][N2][128][KT][2]
   double *acc;        // [d][b/2 + 1][2]
-  int *ctr;           // [0] ticket | done1[U] | done2[U] | acc_cnt[d * G2]
+  int *ctr;           // [0] ticket | done1[U] | done2[U] | acc_cnt[d * NPU * G2]
   int acc_add;
 };
 
@@ -113,8 +115,8 @@ struct Args {
 // j = tile position & 15) — a register target would need a jump per entry.  Entries
 // are sorted by position: the first of a position stores, later ones add.  Returns the
 // mask of positions written.
-template <int OP>
-__device__ __forceinline__ uint32_t pull(const Args &p, int kappa, int t, int item, double *S) {
+template <int OP, bool FOLD>
+__device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, int a, double *S, uint32_t &mask) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)t * 2 + OP;
   const int32_t *off = p.off + row * (p.bsz + 1) + (int64_t)item * 128 + warp * 16;
@@ -123,9 +125,10 @@ __device__ __forceinline__ uint32_t pull(const Args &p, int kappa, int t, int it
   const int64_t kk = (int64_t)kappa * KT + lane;
   const char *Xb = (const char *)(p.X[OP] + p.k0 + (kk < p.K ? kk : p.K - 1));
   const uint32_t ldb = (uint32_t)(p.ld[OP] * 8);
-  double *col = S + ((warp * 16) * 32 + lane) * 2 + OP;
-  uint32_t mask = 0;
-  int prevj = -1;
+  // fold (slice a): an entry of bucket m adds z * w_b^(a m) with z = x (A) or i x (B), so
+  // both parts of its position; otherwise operand OP owns one part
+  double *col = S + ((warp * 16) * 32 + lane) * 2 + (FOLD ? 0 : OP);
+  const uint32_t bmask = (uint32_t)(p.bfull - 1);
   for (int eb = e_lo; eb < e_hi; eb += 8) {
     const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
     uint32_t es[8];
@@ -140,14 +143,21 @@ __device__ __forceinline__ uint32_t pull(const Args &p, int kappa, int t, int it
       if (eb + s < e_hi) {  // warp-uniform
         const int j = (int)((es[s] >> 26) & 15u);
         const double val = (es[s] >> 31) ? -x[s] : x[s];
-        const double old = j == prevj ? col[j * 64] : 0.0;  // 0 + val == val, as a register sum
-        col[j * 64] = old + val;
+        const bool have = (mask >> j) & 1u;
+        if (FOLD) {
+          const uint32_t m = eval_bucket(p.h.f[OP][t], (uint64_t)(es[s] & 0x03ffffffu), p.B);
+          const double2 w = __ldg((const double2 *)p.twb + (((uint32_t)a * m) & bmask));
+          const double cr = OP ? -val * w.y : val * w.x;
+          const double ci = OP ? val * w.x : val * w.y;
+          col[j * 64] = (have ? col[j * 64] : 0.0) + cr;
+          col[j * 64 + 1] = (have ? col[j * 64 + 1] : 0.0) + ci;
+        } else {
+          col[j * 64] = (have ? col[j * 64] : 0.0) + val;  // 0 + val == val, as a register sum
+        }
         mask |= 1u << j;
-        prevj = j;
       }
     }
   }
-  return mask;
 }
 
 // x' = x + y w, y' = x - y w
@@ -234,11 +244,25 @@ __device__ __forceinline__ void post_stages(double (&v)[32]) {
 }
 
 // Pass 1: gather both operands of tile `item`, DFT_N2 over m2, twiddle w_b^(m1 u2), park T in L2
-template <int S1>
-__device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int slot, int item, double *S) {
+template <int S1, bool FOLD>
+__device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int pu, int slot, int idx, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m0 = pull<0>(p, kappa, t, item, S);
-  const uint32_t m1 = pull<1>(p, kappa, t, item, S);
+  // fold: tiles [0, 128) of slice pu, [128, 256) of its partner F - pu (none for the self-paired 0, F/2)
+  int item = idx, half = 0, a = 0;
+  if (FOLD) {
+    half = idx >> 7;
+    item = idx & 127;
+    if (half && (pu == 0 || 2 * pu == p.F)) return;  // block-uniform
+    a = half ? p.F - pu : pu;
+  }
+  uint32_t m0 = 0, m1 = 0;
+  pull<0, FOLD>(p, kappa, t, item, a, S, m0);
+  if (FOLD) {
+    pull<1, true>(p, kappa, t, item, a, S, m0);
+    m1 = m0;
+  } else {
+    pull<1, false>(p, kappa, t, item, a, S, m1);
+  }
   double v[32];
   {
     const double *col = S + ((warp * 16) * 32 + lane) * 2;
@@ -264,19 +288,20 @@ __device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int slo
     const int L = S1 > 4 ? post_pos(warp, r) : ((warp << 4) | r);
     const int u2 = L & ((1 << S1) - 1);
     const int m1 = item * G + (L >> S1);
-    const double2 w = __ldg((const double2 *)p.twb + m1 * u2);
+    // inter-pass twiddle of the slice's 2^LBs-point FFT: w_(b/F)^(m1 u2) = w_b^(F m1 u2)
+    const double2 w = __ldg((const double2 *)p.twb + (int64_t)m1 * u2 * p.F);
     const double re = fma(v[2 * r], w.x, -v[2 * r + 1] * w.y);
     const double im = fma(v[2 * r], w.y, v[2 * r + 1] * w.x);
-    st2_hint(p.Y + ((((int64_t)slot * p.N2 + u2) * 128 + m1) * KT + lane) * 2, re, im, pol);
+    st2_hint(p.Y + (((((int64_t)slot * p.halves + half) * p.N2 + u2) * 128 + m1) * KT + lane) * 2, re, im, pol);
   }
 }
 
 // full 128-point DIT DFT of slice u2 (T[., u2] in L2) into registers; CMP = complement layout
 template <bool CMP>
-__device__ __forceinline__ void slice_dft(const Args &p, int slot, int u2, double (&v)[32], double *S) {
+__device__ __forceinline__ void slice_dft(const Args &p, int slot, int half, int u2, double (&v)[32], double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
-  const double *Ys = p.Y + (((int64_t)slot * p.N2 + u2) * 128) * KT * 2;
+  const double *Ys = p.Y + ((((int64_t)slot * p.halves + half) * p.N2 + u2) * 128) * KT * 2;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const int pn = (warp << 4) | r;
@@ -304,36 +329,54 @@ __device__ __forceinline__ void split_product(double a, double b, double &c, dou
   e = fma(far, fbi, fai * fbr);
 }
 
-// Pass 2: item i2 in [0, N2/2]: the slice pair {i2, N2 - i2}, or the self-paired 0 and N2/2
-__device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int slot, int i2, uint32_t tmem,
+// Pass 2, item i2 of slice-pair unit pu (frequency u = a + F (u2 + N2 u1), u1 = tile position):
+//   pu = 0 (slice 0, self-paired; the whole spectrum when F = 1): i2 in [0, N2/2] pairs rows
+//     i2 and N2 - i2 (Z[-u] at row N2 - i2, position 127 - u1); rows 0 and N2/2 pair with
+//     themselves (position -u1 / 127 - u1, through shared memory);
+//   pu = F/2 (self-paired): i2 < N2/2 pairs rows i2 and N2 - 1 - i2 of the same slice;
+//   otherwise: row i2 of slice pu with row N2 - 1 - i2 of slice F - pu (the unit's second half).
+// The partner row is transformed in the complement layout, so Z[-u] is register-local.
+// Items outside those ranges are empty (the fold units have a fixed item count).
+__device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu, int slot, int i2, uint32_t tmem,
                                         const int *acc_flag, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N2 = p.N2, F = p.F;
+  bool pair = true;
+  int halfB = 0, u2B = N2 - 1 - i2, baseA = pu, baseB = pu;
+  if (pu == 0) {
+    if (2 * i2 > N2) return;  // block-uniform
+    pair = i2 > 0 && 2 * i2 < N2;
+    u2B = N2 - i2;
+  } else if (2 * pu == F) {
+    if (2 * i2 >= N2) return;
+  } else {
+    halfB = 1;
+    baseB = F - pu;
+  }
   int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
-  const int N2 = p.N2;
-  const bool pair = i2 > 0 && 2 * i2 < N2;
   // after the lane reduction this lane owns double `lane` = (register lane >> 1, re/im lane & 1)
   const int u1 = post_pos(warp, lane >> 1);
   int entry = -1;
   bool conj = false;
   if (pair) {
-    if (u1 < 64) entry = i2 + N2 * u1;
-    else { entry = (N2 - i2) + N2 * (127 - u1); conj = true; }
+    if (u1 < 64) entry = baseA + F * (i2 + N2 * u1);
+    else { entry = baseB + F * (u2B + N2 * (127 - u1)); conj = true; }  // b - u holds conj(FA FB (u))
   } else if (i2 == 0) {
-    if (u1 <= 64) entry = N2 * u1;
+    if (u1 <= 64) entry = F * (N2 * u1);
   } else if (u1 <= 63) {
-    entry = i2 + N2 * u1;
+    entry = F * (i2 + N2 * u1);
   }
-  double *a = entry >= 0 ? p.acc + (((int64_t)t * (p.bsz / 2 + 1) + entry) * 2 + (lane & 1)) : nullptr;
+  double *a = entry >= 0 ? p.acc + (((int64_t)t * (p.bfull / 2 + 1) + entry) * 2 + (lane & 1)) : nullptr;
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = (a && (kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   double v[32];
-  slice_dft<false>(p, slot, i2, v, S);
+  slice_dft<false>(p, slot, 0, i2, v, S);
   if (pair) {
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
 #pragma unroll
     for (int c = 0; c < 4; ++c) tmem_st8(tq + 16 * c, v + 8 * c);
     tmem_wait_st();
-    slice_dft<true>(p, slot, N2 - i2, v, S);
+    slice_dft<true>(p, slot, halfB, u2B, v, S);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       double zu[8];
@@ -418,7 +461,7 @@ __device__ __forceinline__ Item decode_item(const Args &p, int64_t pos) {
   return it;
 }
 
-template <int S1>
+template <int S1, bool FOLD>
 __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
   extern __shared__ __align__(16) double S[];  // 64 KB: exchanges, partner lookups, lane reduction
   __shared__ uint32_t s_tmem;
@@ -479,9 +522,13 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
       s_item[1] = it.is_p1;
       s_item[2] = it.u;
       s_item[3] = it.idx;
-      s_item[4] = fdiv(it.u, p.div_d);             // kappa
-      s_item[5] = fmod_(it.u, p.div_d);            // t
+      const int kap = fdiv(it.u, p.div_dnpu);
+      const int rem = it.u - kap * p.d * p.NPU;
+      const int tt = fdiv(rem, p.div_npu);
+      s_item[4] = kap;                             // kappa
+      s_item[5] = tt;                              // t
       s_item[6] = fmod_(it.u, p.div_slot);         // Y slot
+      s_item[7] = rem - tt * p.NPU;                // slice-pair unit
       itn = decode_item(p, nxt);
     }
     tc_fence_before();
@@ -489,14 +536,14 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
     tc_fence_after();
     const int go = s_item[0];
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
-    const int kappa = s_item[4], t = s_item[5], slot = s_item[6];
+    const int kappa = s_item[4], t = s_item[5], slot = s_item[6], pu = s_item[7];
     if (tid == 0 && go) {
       probe(itn);
       nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
     }
     if (!go) break;
-    if (is_p1) p1_item<S1>(p, kappa, t, slot, idx, S);
-    else p2_item(p, kappa, t, slot, idx, tmem, acc_cnt + t * p.G2 + idx, S);
+    if (is_p1) p1_item<S1, FOLD>(p, kappa, t, pu, slot, idx, S);
+    else p2_item(p, kappa, t, pu, slot, idx, tmem, acc_cnt + (t * p.NPU + pu) * p.G2 + idx, S);
     tc_fence_before();
     __syncthreads();  // [B]
     tc_fence_after();
@@ -504,7 +551,7 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
       fence_acq_rel();
       if (is_p1) red_add(done1 + u, 1);
       else {
-        red_add(acc_cnt + t * p.G2 + idx, 1);
+        red_add(acc_cnt + (t * p.NPU + pu) * p.G2 + idx, 1);
         red_add(done2 + u, 1);
       }
     }
@@ -536,18 +583,37 @@ static int init_w128(cudaStream_t s) {
 }  // namespace f2p
 
 bool fft2p_supported(int log2b, int64_t n1, int64_t n2) {
-  return log2b >= 8 && log2b <= 14 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
+  return log2b >= 8 && log2b <= 20 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
 namespace f2p {
-// units in flight: ~2 CTAs per SM need about 2 * num_sms items; a group dispenses G1 + G2
+// Geometry: slices of 2^LBs frequencies (LBs <= 14: one 128 x N2 four-step FFT each);
+// b > 2^14 is folded into F = b / 2^14 slices, grouped into NPU = F/2 + 1 slice-pair units.
+struct Geom {
+  int LBs, S1, N2, F, NPU, halves, G1, G2;
+  int64_t bs;
+};
+static Geom geometry(int log2b) {
+  Geom g;
+  g.LBs = log2b < 14 ? log2b : 14;
+  g.S1 = g.LBs - 7;
+  g.N2 = 1 << g.S1;
+  g.bs = (int64_t)1 << g.LBs;
+  g.F = 1 << (log2b - g.LBs);
+  if (g.F == 1) {
+    g.NPU = 1; g.halves = 1; g.G1 = g.N2; g.G2 = g.N2 / 2 + 1;
+  } else {  // fixed item counts per unit (empty items for the self-paired slices)
+    g.NPU = g.F / 2 + 1; g.halves = 2; g.G1 = 2 * 128; g.G2 = 128;
+  }
+  return g;
+}
+
 // units in flight: about 4 items per SM (2 CTAs x 2) must be dispensable, and a
-// group dispenses G1 + G2; the T ring ((lag + 2) slots of b x 32 complex) stays within ~64 MB
-static int lag_for(int log2b) {
-  const int b7 = 1 << (log2b - 7);
-  const int grp = b7 + b7 / 2 + 1;
+// group dispenses G1 + G2; the T ring ((lag + 2) slots) stays within ~64 MB of L2
+static int lag_for(const Geom &g) {
+  const int grp = g.G1 + g.G2;
   int lag = (4 * num_sms() + grp - 1) / grp;
-  const int cap = (int)(((int64_t)64 << 20) / (((int64_t)1 << log2b) * KT * 16)) - 2;
+  const int cap = (int)(((int64_t)64 << 20) / (g.halves * g.bs * KT * 16)) - 2;
   if (lag > cap) lag = cap;
   return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
 }
@@ -555,19 +621,18 @@ static int lag_for(int log2b) {
 
 int64_t fft2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   using f2p::pad256;
+  const f2p::Geom g = f2p::geometry(log2b);
   const int64_t b = (int64_t)1 << log2b;
   const int64_t nmax = n1 > n2 ? n1 : n2;
   const int64_t ntiles = (K + f2p::KT - 1) / f2p::KT;
-  const int64_t U = ntiles * d;
-  const int64_t N2 = b >> 7;
-  const int64_t G2 = N2 / 2 + 1;
+  const int64_t U = ntiles * d * g.NPU;
   int64_t w = 0;
-  w += pad256((int64_t)d * 2 * (b + 1) * 4);                 // off
-  w += pad256((int64_t)d * 2 * b * 4);                       // cnt / fill
-  w += pad256((int64_t)d * 2 * nmax * 4);                    // ent
-  w += pad256(b * 16);                                       // twiddles w_b^x
-  w += pad256((int64_t)(f2p::lag_for(log2b) + 2) * b * f2p::KT * 16);  // T ring
-  w += pad256((1 + 2 * U + (int64_t)d * G2) * 4);            // counters
+  w += pad256((int64_t)d * 2 * (g.bs + 1) * 4);                // off
+  w += pad256((int64_t)d * 2 * g.bs * 4);                      // cnt / fill
+  w += pad256((int64_t)d * 2 * nmax * 4);                      // ent
+  w += pad256(b * 16);                                         // twiddles w_b^x
+  w += pad256((int64_t)(f2p::lag_for(g) + 2) * g.halves * g.bs * f2p::KT * 16);  // T ring
+  w += pad256((1 + 2 * U + (int64_t)d * g.NPU * g.G2) * 4);    // counters
   return w;
 }
 
@@ -576,10 +641,12 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
                      cudaStream_t s) {
   using namespace f2p;
   const int d = h.d, log2b = h.log2b;
+  const Geom g = geometry(log2b);
   const int64_t b = (int64_t)1 << log2b;
+  const int64_t bs = g.bs;
   const int64_t K = k1 - k0;
   const int64_t nmax = n1 > n2 ? n1 : n2;
-  const int S1 = log2b - 7;
+  const int S1 = g.S1;
   if (lda >= ((int64_t)1 << 28) || ldb >= ((int64_t)1 << 28)) {
     set_error("operand row stride too large for the two-pass kernel");
     return SMM_ERR_INVALID;
@@ -590,23 +657,21 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   }
   char *q = ws;
   int32_t *off = (int32_t *)q;
-  q += pad256((int64_t)d * 2 * (b + 1) * 4);
+  q += pad256((int64_t)d * 2 * (bs + 1) * 4);
   int32_t *cnt = (int32_t *)q;
-  q += pad256((int64_t)d * 2 * b * 4);
+  q += pad256((int64_t)d * 2 * bs * 4);
   uint32_t *ent = (uint32_t *)q;
   q += pad256((int64_t)d * 2 * nmax * 4);
   double *twb = (double *)q;
   q += pad256(b * 16);
   double *Y = (double *)q;
-  const int lag = lag_for(log2b);
+  const int lag = lag_for(g);
   const int nslot = lag + 2;
-  q += pad256((int64_t)nslot * b * KT * 16);
+  q += pad256((int64_t)nslot * g.halves * bs * KT * 16);
   int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;
-  const int64_t U = ntiles * d;
-  const int N2 = (int)(b >> 7);
-  const int G1 = (int)(b >> 7);  // 128-position gather tiles per unit
-  const int G2 = N2 / 2 + 1;     // slice pairs + the two self-paired slices
+  const int64_t U = ntiles * d * g.NPU;
+  const int N2 = g.N2, G1 = g.G1, G2 = g.G2;
   const size_t acc_bytes = (size_t)d * (size_t)(b / 2 + 1) * 16;
   if (K <= 0) {
     if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, acc_bytes, s), "acc memset");
@@ -621,26 +686,26 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   twiddle_b_kernel<<<(unsigned)ceil_div(b, 256) > 1024 ? 1024 : (unsigned)ceil_div(b, 256), 256, 0, s>>>(twb, log2b);
   SMM_LAUNCH_CHECK("twiddle_b_kernel");
   // plan: CSR by bit-reversed tile position
-  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * bs * 4, s), "csr memset");
   const int64_t nin = (int64_t)d * (n1 + n2);
   int64_t blocks = ceil_div(nin, 256);
   if (blocks > 8192) blocks = 8192;
   if (nin > 0) {
-    csr_count_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, b, S1);
+    csr_count_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, bs, S1);
     SMM_LAUNCH_CHECK("csr_count_fft");
   }
-  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, b);
+  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, bs);
   SMM_LAUNCH_CHECK("csr_scan_kernel");
-  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * b * 4, s), "csr memset");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * bs * 4, s), "csr memset");
   if (nin > 0) {
-    csr_fill_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, b, S1);
+    csr_fill_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, bs, S1);
     SMM_LAUNCH_CHECK("csr_fill_fft");
-    int64_t sb = ceil_div((int64_t)d * 2 * b, 256);
+    int64_t sb = ceil_div((int64_t)d * 2 * bs, 256);
     if (sb > 8192) sb = 8192;
-    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, b, d * 2);
+    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, bs, d * 2);
     SMM_LAUNCH_CHECK("csr_sort_kernel");
   }
-  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * G2) * 4, s), "counter memset");
+  SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * g.NPU * G2) * 4, s), "counter memset");
   Args p;
   p.h = h;
   p.X[0] = xa;
@@ -655,7 +720,11 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   p.G2 = G2;
   p.U = (int)U;
   p.d = d;
-  p.div_d = make_fastdiv((uint32_t)d);
+  p.F = g.F;
+  p.NPU = g.NPU;
+  p.halves = g.halves;
+  p.div_dnpu = make_fastdiv((uint32_t)(d * g.NPU));
+  p.div_npu = make_fastdiv((uint32_t)g.NPU);
   p.div_slot = make_fastdiv((uint32_t)nslot);
   p.lag = lag;
   p.nslot = nslot;
@@ -663,7 +732,8 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   p.off = off;
   p.ent = ent;
   p.nmax = nmax;
-  p.bsz = b;
+  p.bsz = bs;
+  p.bfull = b;
   p.twb = twb;
   p.Y = Y;
   p.acc = acc;
@@ -671,14 +741,15 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   p.acc_add = acc_add ? 1 : 0;
   const size_t smem = (size_t)8 * 32 * 32 * 8;
   const int G = 2 * num_sms();
-  switch (S1) {
-#define F2P_LAUNCH(SS)                                                                                 \
-  case SS:                                                                                            \
-    SMM_CUDA_TRY(cudaFuncSetAttribute(fft2p_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+#define F2P_LAUNCH(SS, FD)                                                                             \
+  case SS + 8 * FD:                                                                                   \
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fft2p_kernel<SS, FD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
                  "fft2p smem");                                                                       \
-    fft2p_kernel<SS><<<G, THREADS, smem, s>>>(p);                                                     \
+    fft2p_kernel<SS, FD><<<G, THREADS, smem, s>>>(p);                                                 \
     break;
-    F2P_LAUNCH(1) F2P_LAUNCH(2) F2P_LAUNCH(3) F2P_LAUNCH(4) F2P_LAUNCH(5) F2P_LAUNCH(6) F2P_LAUNCH(7)
+  switch (S1 + 8 * (g.F > 1 ? 1 : 0)) {
+    F2P_LAUNCH(1, 0) F2P_LAUNCH(2, 0) F2P_LAUNCH(3, 0) F2P_LAUNCH(4, 0) F2P_LAUNCH(5, 0) F2P_LAUNCH(6, 0)
+    F2P_LAUNCH(7, 0) F2P_LAUNCH(7, 1)
 #undef F2P_LAUNCH
     default:
       set_error("two-pass fft kernel: unsupported width");

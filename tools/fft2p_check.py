@@ -12,7 +12,8 @@ from paper_2601_09477_b200 import _device  # noqa: E402
 
 bad = 0
 for log2b, n1, m, n2, d in ((8, 300, 70, 200, 3), (10, 500, 100, 400, 5), (12, 700, 33, 650, 3), (14, 1000, 64, 900, 3),
-                            (9, 64, 40, 80, 1), (11, 2000, 96, 1500, 3), (13, 300, 50, 300, 5)):
+                            (9, 64, 40, 80, 1), (11, 2000, 96, 1500, 3), (13, 300, 50, 300, 5),
+                            (15, 500, 40, 450, 3), (16, 700, 33, 650, 3), (17, 300, 64, 300, 1), (18, 400, 32, 350, 3)):
     rng = np.random.default_rng(log2b)
     a = rng.standard_normal((n1, m))
     bm = rng.standard_normal((m, n2))
