@@ -262,7 +262,7 @@ def test_transforms_api(transforms_golden):
         P.fwht_inplace(np.zeros(6))
 
 
-@pytest.mark.parametrize("transform,log2b", [("fwht", 12), ("fwht", 6), ("fft", 10)])
+@pytest.mark.parametrize("transform,log2b", [("fwht", 12), ("fwht", 6), ("fft", 10), ("fft", 15)])
 def test_host_streamed_compress(transform, log2b):
     # host operands are uploaded in k-slabs while earlier slabs compute; every slab
     # after the first runs in accumulate mode.  The two-pass FWHT kernel continues
@@ -342,3 +342,20 @@ def test_compress_seeds_equals_per_seed_compress(transform, log2b, d):
     many_h = P.compress_seeds(a.cpu(), b.cpu(), p, seeds[:3])
     for x, y in zip(many_h, many[:3]):
         assert np.max(np.abs(x.polys - y.polys)) <= 1e-12 * np.max(np.abs(y.polys))
+
+
+@pytest.mark.parametrize("log2b,n1,m,n2,d", [(8, 300, 70, 200, 3), (11, 2000, 96, 1500, 3), (13, 300, 50, 300, 5),
+                                             (14, 1000, 64, 900, 3), (15, 500, 40, 450, 3), (16, 700, 33, 650, 3),
+                                             (18, 400, 32, 350, 3)])
+def test_two_pass_fft_against_oracle(log2b, n1, m, n2, d):
+    # fft2p: four-step FFT (b <= 2^14) and its frequency fold (b > 2^14), partial k-tiles,
+    # rectangular operands, against the oracle (reference algorithm) at 1e-12 relative
+    rng = np.random.default_rng(log2b)
+    a = rng.standard_normal((n1, m))
+    bm = rng.standard_normal((m, n2))
+    words = O.draw_words(log2b + 100, d, 1 << log2b)
+    acc = _device.compress_accumulate(torch.from_numpy(a).cuda(), torch.from_numpy(bm).cuda(), words, d, log2b, "fft",
+                                      0, m, a_layout=_device.KMINOR, b_layout=_device.KMAJOR)
+    polys = _device.finalize(acc, d, log2b, "fft").cpu().numpy()
+    ref = O.compress(a, bm, b=1 << log2b, d=d, words=words, transform="fft", seed=0, threads=8)
+    assert np.abs(polys - ref).max() <= 1e-12 * np.abs(ref).max()
