@@ -255,10 +255,6 @@ __device__ __forceinline__ void reg_fwht32(double (&v)[32], int qlo, int qhi) {
   }
 }
 
-#define SMM_CASE(J) \
-  case J:           \
-    v[J] += val;    \
-    break;
 
 // Pass 1: pull the 256 buckets [blk*256, blk*256+256) of operand op for the
 // 32 inner indices of k-tile kappa, FWHT over the 8 low bucket bits, write Y.
