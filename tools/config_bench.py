@@ -25,7 +25,8 @@ from paper_2601_09477_b200 import workloads as W  # noqa: E402
 FP64_OPS_PEAK = 18.52e12  # DADD / DFMA per second (profiles/r01_microbench.txt)
 DEFAULT = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_b12_d3_nnz512_fwht", "cfg5_b12_d5_nnz512_fft",
            "cfg5_b14_d9_nnz512_fwht", "cfg5_b14_d9_nnz512_fft", "cfg5_b16_d9_nnz512_fwht",
-           "cfg5_b16_d3_nnz512_fft", "cfg5_b18_d3_nnz512_fwht", "cfg5_b20_d3_nnz512_fwht"]
+           "cfg5_b16_d3_nnz512_fft", "cfg5_b18_d3_nnz512_fwht", "cfg5_b18_d3_nnz512_fft",
+           "cfg5_b20_d3_nnz512_fwht", "cfg5_b20_d3_nnz512_fft"]
 
 
 def fp64_ops(n, b, d, transform):
