@@ -182,6 +182,21 @@ def _config(args, n, b, d):
             "l2": "operands (2 x 2 GiB) exceed the 126 MB L2; no flush needed between steps"}
 
 
+L2_WRITE_TBS = 7.57  # L2-resident store bandwidth (tools/microbench.cu)
+L2_READ_TBS = 17.5   # L2-resident read bandwidth
+GATHERS_PER_S = 294.4e9  # random 8-byte gathers (1.00 per clk per SM)
+
+
+def _l2_view(kl: int, b: int, d: int, t_ms: float) -> dict:
+    lb = b.bit_length() - 1
+    bs = 1 << min(lb, 16)              # two-pass slice size (fold above 2^16)
+    units = -(-kl // 32) * d * (b // bs)
+    y = 2 * units * bs * 32 * 8        # both operands, one 32-wide k-tile per unit
+    floor_ms = (y / (L2_WRITE_TBS * 1e12) + y / (L2_READ_TBS * 1e12)) * 1e3
+    return {"y_bytes_written": y, "y_bytes_read": y, "floor_ms": floor_ms, "frac": floor_ms / t_ms,
+            "peaks_tbs": {"write": L2_WRITE_TBS, "read": L2_READ_TBS}}
+
+
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args) -> None:
     import torch
@@ -284,7 +299,15 @@ def run_ours(args) -> None:
                         "peak_gbs": _peaks().get("hbm_gbs"),
                         "frac": hbm_bytes / (t_comp * 1e-3) / 1e9 / _peaks().get("hbm_gbs", 6650.0)},
                 "extract": {"ms": t_extract, "algorithmic_bytes": 8 * (r1 - r0) * n,
-                            "achieved_gbs": 8 * (r1 - r0) * n / (t_extract * 1e-3) / 1e9}}
+                            "achieved_gbs": 8 * (r1 - r0) * n / (t_extract * 1e-3) / 1e9,
+                            # d random 8-byte gathers per estimate, one L1 line lookup each (1/clk/SM,
+                            # profiles/r01_microbench.txt "gather8"): the binding resource
+                            "gathers": d * (r1 - r0) * n,
+                            "gather_floor_ms": d * (r1 - r0) * n / GATHERS_PER_S * 1e3,
+                            "frac_of_gather_floor": d * (r1 - r0) * n / GATHERS_PER_S * 1e3 / t_extract},
+                # the pass-1 -> pass-2 intermediate Y crosses L2 once per element and operand:
+                # written at <= 7.57 TB/s and read at <= 17.5 TB/s (measured, profiles/r01_microbench.txt)
+                "l2": _l2_view(kl, b, d, t_comp)}
     traffic_file = ROOT / "profiles" / "r01_compress_dram_bytes.json"
     if traffic_file.exists():
         try:

@@ -265,6 +265,30 @@ __global__ void k_dmma16(double* out, int iters) {
   if (t == 1.2345) out[0] = t;
 }
 
+// ---------------- random 8-byte gathers from an L2-resident table (the extraction pattern) -----------------
+__global__ void k_gather(const double *tab, uint32_t mask, int iters, double *out) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      x = x * 1664525u + 1013904223u;
+      v[j] = __ldg(tab + ((x >> 7) & mask));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += v[j];
+  }
+  if (acc == 123.0) out[0] = acc;
+}
+
+// ---------------- coalesced 8-byte stores into an L2-resident buffer (the pass-1 Y pattern) -----------------
+__global__ void k_write(double *buf, size_t n, int reps) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) buf[i] = (double)(i + r);
+}
+
 int main() {
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
   g_sms = prop.multiProcessorCount;
@@ -316,6 +340,24 @@ int main() {
       printf("read %4zu MB x%d: %.2f TB/s\n", mb, reps, (double)bytes * reps / ms / 1e9);
       CK(cudaFree(p));
     }
+  }
+  {
+    // 5 x 2^16 doubles (2.6 MB, cfg3's polys) and 2^20 doubles (8 MB)
+    for (uint32_t n : {5u * 65536u, 1u << 20}) {
+      uint32_t m = 1; while (m < n) m <<= 1; m -= 1;
+      double *tab; CK(cudaMalloc(&tab, (size_t)(m + 1) * 8)); CK(cudaMemset(tab, 0, (size_t)(m + 1) * 8));
+      int it = 256;
+      float ms = time_ms([&] { k_gather<<<g_sms * 8, 256>>>(tab, m, it, out); });
+      double g = (double)g_sms * 8 * 256 * it * 8;
+      printf("gather8 %4.1f MB: %.1f G/s (%.2f gathers/clk/SM, random 8-byte loads, one line each)\n",
+             (m + 1) * 8 / 1048576.0, g / ms / 1e6, g / (ms * 1e-3) / g_sms / (clk_khz * 1e3));
+      CK(cudaFree(tab));
+    }
+    size_t bytes = (size_t)64 << 20;
+    double *w; CK(cudaMalloc(&w, bytes));
+    float ms = time_ms([&] { k_write<<<g_sms * 8, 512>>>(w, bytes / 8, 20); });
+    printf("write  64 MB x20: %.2f TB/s (L2-resident stores)\n", (double)bytes * 20 / ms / 1e9);
+    CK(cudaFree(w));
   }
   {
     CK(cudaFuncSetAttribute(k_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
