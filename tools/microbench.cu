@@ -289,6 +289,33 @@ __global__ void k_write(double *buf, size_t n, int reps) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) buf[i] = (double)(i + r);
 }
 
+__global__ void k_write2(double2 *buf, size_t n, int reps) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride)
+      buf[i] = make_double2((double)(i + r), 1.0);
+}
+
+// one 64 KB bulk copy (TMA engine) from shared memory per iteration and CTA
+__global__ void k_bulk_store(char *buf, size_t bytes, int reps) {
+  extern __shared__ __align__(128) char smb[];
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) ((int *)smb)[i] = i;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const size_t tiles = bytes / 65536;
+    for (int r = 0; r < reps; ++r)
+      for (size_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 65536;" ::"l"(buf + t * 65536),
+                     "r"((uint32_t)__cvta_generic_to_shared(smb))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+      }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 int main() {
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
   g_sms = prop.multiProcessorCount;
@@ -356,7 +383,12 @@ int main() {
     size_t bytes = (size_t)64 << 20;
     double *w; CK(cudaMalloc(&w, bytes));
     float ms = time_ms([&] { k_write<<<g_sms * 8, 512>>>(w, bytes / 8, 20); });
-    printf("write  64 MB x20: %.2f TB/s (L2-resident stores)\n", (double)bytes * 20 / ms / 1e9);
+    printf("write  64 MB x20: %.2f TB/s (L2-resident stores, 8 B/thread)\n", (double)bytes * 20 / ms / 1e9);
+    ms = time_ms([&] { k_write2<<<g_sms * 8, 512>>>((double2 *)w, bytes / 16, 20); });
+    printf("write2 64 MB x20: %.2f TB/s (L2-resident stores, 16 B/thread)\n", (double)bytes * 20 / ms / 1e9);
+    CK(cudaFuncSetAttribute(k_bulk_store, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    ms = time_ms([&] { k_bulk_store<<<g_sms * 2, 128, 65536>>>((char *)w, bytes, 20); });
+    printf("bulk   64 MB x20: %.2f TB/s (L2-resident cp.async.bulk stores from smem)\n", (double)bytes * 20 / ms / 1e9);
     CK(cudaFree(w));
   }
   {
