@@ -252,8 +252,7 @@ __device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int pu,
   if (FOLD) {
     half = idx >> 7;
     item = idx & 127;
-    if (half && (pu == 0 || 2 * pu == p.F)) return;  // block-uniform
-    a = half ? p.F - pu : pu;
+    a = half ? (pu == 0 ? p.F / 2 : p.F - pu) : pu;  // unit 0 = the self-paired slices {0, F/2}
   }
   uint32_t m0 = 0, m1 = 0;
   pull<0, FOLD>(p, kappa, t, item, a, S, m0);
@@ -330,26 +329,32 @@ __device__ __forceinline__ void split_product(double a, double b, double &c, dou
 }
 
 // Pass 2, item i2 of slice-pair unit pu (frequency u = a + F (u2 + N2 u1), u1 = tile position):
-//   pu = 0 (slice 0, self-paired; the whole spectrum when F = 1): i2 in [0, N2/2] pairs rows
+//   unit 0, i2 in [0, N2/2]: slice 0 (self-paired; the whole spectrum when F = 1) pairs rows
 //     i2 and N2 - i2 (Z[-u] at row N2 - i2, position 127 - u1); rows 0 and N2/2 pair with
 //     themselves (position -u1 / 127 - u1, through shared memory);
-//   pu = F/2 (self-paired): i2 < N2/2 pairs rows i2 and N2 - 1 - i2 of the same slice;
-//   otherwise: row i2 of slice pu with row N2 - 1 - i2 of slice F - pu (the unit's second half).
+//   unit 0, i2 > N2/2 (fold only): slice F/2 (self-paired, the unit's second half) pairs rows
+//     j = i2 - N2/2 - 1 and N2 - 1 - j;
+//   unit pu > 0: row i2 of slice pu with row N2 - 1 - i2 of slice F - pu (the second half).
 // The partner row is transformed in the complement layout, so Z[-u] is register-local.
-// Items outside those ranges are empty (the fold units have a fixed item count).
 __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu, int slot, int i2, uint32_t tmem,
                                         const int *acc_flag, double *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N2 = p.N2, F = p.F;
   bool pair = true;
-  int halfB = 0, u2B = N2 - 1 - i2, baseA = pu, baseB = pu;
+  int halfA = 0, rowA = i2, halfB = 0, u2B = N2 - 1 - i2, baseA = pu, baseB = pu;
   if (pu == 0) {
-    if (2 * i2 > N2) return;  // block-uniform
-    pair = i2 > 0 && 2 * i2 < N2;
-    u2B = N2 - i2;
-  } else if (2 * pu == F) {
-    if (2 * i2 >= N2) return;
+    if (2 * i2 <= N2) {  // slice 0
+      pair = i2 > 0 && 2 * i2 < N2;
+      u2B = N2 - i2;
+    } else {  // fold: slice F/2 in the unit's second half, rows j and N2 - 1 - j
+      const int j = i2 - (N2 / 2 + 1);
+      halfA = halfB = 1;
+      rowA = j;
+      u2B = N2 - 1 - j;
+      baseA = baseB = F / 2;
+    }
   } else {
+    if (i2 >= N2) return;  // block-uniform: the spare item of a slice-pair unit
     halfB = 1;
     baseB = F - pu;
   }
@@ -359,7 +364,7 @@ __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu,
   int entry = -1;
   bool conj = false;
   if (pair) {
-    if (u1 < 64) entry = baseA + F * (i2 + N2 * u1);
+    if (u1 < 64) entry = baseA + F * (rowA + N2 * u1);
     else { entry = baseB + F * (u2B + N2 * (127 - u1)); conj = true; }  // b - u holds conj(FA FB (u))
   } else if (i2 == 0) {
     if (u1 <= 64) entry = F * (N2 * u1);
@@ -370,7 +375,7 @@ __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu,
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = (a && (kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   double v[32];
-  slice_dft<false>(p, slot, 0, i2, v, S);
+  slice_dft<false>(p, slot, halfA, rowA, v, S);
   if (pair) {
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
 #pragma unroll
@@ -603,7 +608,9 @@ static Geom geometry(int log2b) {
   if (g.F == 1) {
     g.NPU = 1; g.halves = 1; g.G1 = g.N2; g.G2 = g.N2 / 2 + 1;
   } else {  // fixed item counts per unit (empty items for the self-paired slices)
-    g.NPU = g.F / 2 + 1; g.halves = 2; g.G1 = 2 * 128; g.G2 = 128;
+    // units: {0, F/2} and the pairs {a, F - a}; pass 2: N2 rows per pair unit (+1 spare),
+    // N2/2 + 1 rows of slice 0 and N2/2 of slice F/2 in unit 0
+    g.NPU = g.F / 2; g.halves = 2; g.G1 = 2 * 128; g.G2 = 128 + 1;
   }
   return g;
 }
