@@ -277,8 +277,23 @@ __device__ __forceinline__ PullHead pull_head(const TwoPassArgs &p, int t, int o
   return h;
 }
 
+// first-batch gathers of an operand, issued ahead of its pull (lanes 0-7 of the head hold the entries)
+__device__ __forceinline__ void gather_first(const TwoPassArgs &p, int kappa, int op, const PullHead &hd,
+                                             double (&x)[8]) {
+  const int64_t kk = (int64_t)kappa * KT + (threadIdx.x & 31);
+  const char *Xb = (const char *)(p.X[op] + p.k0 + (kk < p.K ? kk : p.K - 1));
+  const uint32_t ldb = (uint32_t)(p.ld[op] * 8);
+  const int cnt = hd.e_hi - hd.e_lo;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const uint32_t e = __shfl_sync(0xffffffffu, hd.first, s);
+    x[s] = s < cnt ? __ldg((const double *)(Xb + (uint64_t)(e & 0x03ffffffu) * ldb)) : 0.0;
+  }
+}
+
 __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
-                                           double *S, const PullHead &hd) {
+                                           double *S, const PullHead &hd, double (&xpre)[8], bool have_pre,
+                                           const PullHead *next) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // lanes past the end of the inner range read a valid element and are zeroed after the pull
   const int64_t kk = (int64_t)kappa * KT + lane;
@@ -305,11 +320,16 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
     double x[8];
 #pragma unroll
     for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
+    if (have_pre && eb == e_lo) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      x[s] = eb + s < e_hi
-                 ? __ldg((const double *)(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb))
-                 : 0.0;
+      for (int s = 0; s < 8; ++s) x[s] = xpre[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        x[s] = eb + s < e_hi
+                   ? __ldg((const double *)(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb))
+                   : 0.0;
+    }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       if (eb + s < e_hi) {  // warp-uniform
@@ -344,6 +364,8 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
   for (int r = 0; r < 32; ++r) v[r] = S[((r & 7) * 32 + (warp + 8 * (r >> 3))) * 32 + lane];
   reg_fwht32(v, 0, 3);  // bucket bits 5-7
   PROF_MARK(6);
+  // the other operand's first gathers go out before this operand's 64 KB of Y stores
+  if (next) gather_first(p, kappa, 1, *next, xpre);
   double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 256) * KT + lane;
   const uint64_t pol = policy_evict_last();
 #pragma unroll
@@ -357,9 +379,10 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
 __device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double *S,
                                         const PullHead &hd0) {
   const PullHead hd1 = pull_head(p, t, 1, blk);  // operand 1's head lands while operand 0 computes
-  p1_operand(p, kappa, t, a, slot, 0, blk, S, hd0);
+  double xpre[8];
+  p1_operand(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
   __syncthreads();  // every warp has read operand 0's exchange data from S
-  p1_operand(p, kappa, t, a, slot, 1, blk, S, hd1);
+  p1_operand(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
 }
 
 // Pass 2: for slice s (256 buckets: every high-bit value x 2^(8-hb) low values)
