@@ -28,6 +28,8 @@
  *   smm_fwht_batched         transforms.py:37-49 / 100-127 (fwht_inplace, xor_convolve)
  *   smm_fft_batched          transforms.py:52-74 / 130-175 (fft_forward, fft_inverse,
  *                            cyclic_convolve)
+ *   smm_query                sketch.py:343-372 (sketch_estimates / decompress_entry,
+ *                            batched over (i, j) pairs on the device-resident sketch)
  *   smm_copy2d               np.ascontiguousarray(a, dtype=float64) (sketch.py:282-286):
  *                            the host->device move of the operands, done per k-slab so
  *                            uploads overlap the compress kernel
@@ -128,6 +130,12 @@ int smm_extract(int variant, const double *polys, const uint64_t *words_host, in
  * thresholding loop of experiments.py:136-168. */
 int smm_hh_pairs(const void *workspace, int64_t n2, int64_t r0, int64_t r1, int64_t *hh_pairs, int64_t hh_cap,
                  void *stream);
+
+/* Per-entry estimates for `count` (i, j) pairs (ij [dev]: int64 pairs; the caller
+ * range-checks them against n1 x n2, as sketch.py:352-355 does): est [dev] the
+ * median, reps [dev, nullable] the d signed per-repetition values (count x d). */
+int smm_query(int variant, const double *polys, const uint64_t *words_host, int d, int log2b, int64_t n1,
+              int64_t n2, const int64_t *ij, int64_t count, double *est, double *reps, void *stream);
 
 /* Number of kernels this library has launched in the process (monotone counter;
  * bench/evidence only). */

@@ -255,6 +255,21 @@ def extract(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant:
     return est, count, pairs
 
 
+def query(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str, n1: int, n2: int,
+          ij: torch.Tensor, want_reps: bool = False):
+    """Median estimates (and optionally the d per-repetition values) at int64 (i, j) pairs."""
+    lib = _lib.load()
+    dev = polys.device
+    ij = ij.to(device=dev, dtype=torch.int64).contiguous()
+    count = ij.shape[0]
+    est = torch.empty(count, dtype=torch.float64, device=dev)
+    reps = torch.empty((count, d), dtype=torch.float64, device=dev) if want_reps else None
+    words, wp = words_ptr(words)
+    _lib.check(lib.smm_query(_lib.VARIANT[variant], ptr(polys), wp, d, log2b, n1, n2, ptr(ij), count, ptr(est),
+                             ptr(reps), stream_ptr(dev)))
+    return est, reps
+
+
 def extract_host(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str, n1: int, n2: int,
                  r0: int, r1: int, thr: float, strict: bool, est_host: torch.Tensor, block_rows: int | None = None):
     """Rows [r0, r1) of the estimates into a host tensor, in row blocks: block q+1

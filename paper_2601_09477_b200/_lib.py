@@ -37,6 +37,7 @@ EXPORTS = (
     "smm_extract_workspace",
     "smm_extract",
     "smm_hh_pairs",
+    "smm_query",
     "smm_kernel_launches",
     "smm_transpose",
     "smm_copy2d",
@@ -85,6 +86,7 @@ def load():
             "smm_kernel_launches": ([], I64),
             "smm_transpose": ([P, I64, I64, I64, P, I64, P], I),
             "smm_copy2d": ([P, I64, P, I64, I64, I64, P], I),
+            "smm_query": ([I, P, P, I, I, I64, I64, P, I64, P, P, P], I),
             "smm_fwht_batched": ([P, I64, I, D, P], I),
             "smm_fft_batched": ([P, I64, I, I, D, P], I),
         }

@@ -31,6 +31,8 @@ int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1,
             double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
             int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s);
 int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs, int64_t cap, cudaStream_t s);
+int query(int variant, const SketchHashes &h, const double *polys, const int64_t *ij, int64_t count, double *est,
+          double *reps, cudaStream_t s);
 int64_t launches();
 int transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out, int64_t ld_out,
               cudaStream_t s);
@@ -262,6 +264,19 @@ int smm_hh_pairs(const void *workspace, int64_t n2, int64_t r0, int64_t r1, int6
   SMM_REQUIRE(r0 >= 0 && r1 >= r0 && n2 >= 0 && hh_cap >= 0, "bad ranges");
   SMM_REQUIRE(hh_cap == 0 || hh_pairs != nullptr, "hh_pairs is NULL");
   return smm::hh_pairs(workspace, n2, r0, r1, hh_pairs, hh_cap, (cudaStream_t)stream);
+}
+
+int smm_query(int variant, const double *polys, const uint64_t *words_host, int d, int log2b, int64_t n1, int64_t n2,
+              const int64_t *ij, int64_t count, double *est, double *reps, void *stream) {
+  int rc = check_sketch(variant, d, log2b, true);
+  if (rc) return rc;
+  SMM_REQUIRE(count >= 0, "count < 0");
+  SMM_REQUIRE(count == 0 || (polys != nullptr && words_host != nullptr && ij != nullptr && est != nullptr),
+              "NULL argument");
+  SMM_REQUIRE(n1 <= ((int64_t)1 << 32) && n2 <= ((int64_t)1 << 32), "keys must fit in 32 bits");
+  SketchHashes h;
+  load_hashes(h, words_host, d, log2b);
+  return query(variant, h, polys, ij, count, est, reps, (cudaStream_t)stream);
 }
 
 int64_t smm_kernel_launches(void) { return launches(); }

@@ -190,6 +190,47 @@ __global__ void hh_write_kernel(const uint32_t *mask, int64_t mask_ld, const int
   }
 }
 
+// Per-entry queries (sketch.py:343-372 sketch_estimates / decompress_entry) for a batch
+// of (i, j) pairs: one thread per query; est[q] = median, reps[q * d + t] (nullable) the
+// d signed per-repetition estimates in repetition order.
+__global__ void query_kernel(SketchHashes h, const double *polys, const int64_t *ij, int64_t count, int xor_combine,
+                             double *est, double *reps) {
+  const int d = h.d;
+  const int log2b = h.log2b;
+  const uint32_t bmask = (uint32_t)(((uint64_t)1 << log2b) - 1);
+  const int64_t b = (int64_t)1 << log2b;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)ij[2 * q], j = (uint64_t)ij[2 * q + 1];
+    double v[SMM_MAX_DEPTH];
+    for (int t = 0; t < d; ++t) {
+      const uint32_t a = eval_bucket(h.f[0][t], i, log2b), c = eval_bucket(h.f[1][t], j, log2b);
+      const uint32_t idx = xor_combine ? (a ^ c) : ((a + c) & bmask);
+      double x = polys[t * b + idx];
+      x *= eval_signbit(h.f[2][t], i) ? -1.0 : 1.0;  // eval_sign(s1) * eval_sign(s2) * polys (sketch.py:364-366)
+      x *= eval_signbit(h.f[3][t], j) ? -1.0 : 1.0;
+      v[t] = x;
+      if (reps) reps[q * d + t] = x;
+    }
+    for (int a2 = 1; a2 < d; ++a2) {  // insertion sort: the exact middle order statistic
+      const double key = v[a2];
+      int k = a2 - 1;
+      while (k >= 0 && v[k] > key) { v[k + 1] = v[k]; --k; }
+      v[k + 1] = key;
+    }
+    est[q] = v[(d - 1) / 2];
+  }
+}
+
+int query(int variant, const SketchHashes &h, const double *polys, const int64_t *ij, int64_t count, double *est,
+          double *reps, cudaStream_t s) {
+  if (count <= 0) return SMM_OK;
+  int64_t blocks = ceil_div(count, 128);
+  if (blocks > 4096) blocks = 4096;
+  query_kernel<<<(unsigned)blocks, 128, 0, s>>>(h, polys, ij, count, variant == SMM_VARIANT_FWHT ? 1 : 0, est, reps);
+  SMM_LAUNCH_CHECK("query_kernel");
+  return SMM_OK;
+}
+
 int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs, int64_t cap, cudaStream_t s);
 
 int64_t extract_workspace(int64_t n2, int64_t r0, int64_t r1) {

@@ -375,6 +375,34 @@ def decompress_entry(sketch: ProductSketch, i: int, j: int) -> float:
     return float(np.median(sketch_estimates(sketch, i, j)))
 
 
+def decompress_entries(sketch: ProductSketch, ij, *, with_estimates: bool = False, device=None,
+                       as_numpy: bool = True):
+    """Batched per-entry queries on the device-resident sketch: the median estimate
+    of every (i, j) pair in ``ij`` (shape (q, 2)), equal to ``decompress_entry`` per
+    pair; with ``with_estimates`` also the (q, d) per-repetition values of
+    ``sketch_estimates`` (sketch.py:350-372)."""
+    import torch
+
+    from . import _device
+
+    arr = ij if isinstance(ij, torch.Tensor) else torch.as_tensor(np.asarray(ij, dtype=np.int64))
+    if arr.ndim != 2 or arr.shape[1] != 2:
+        raise InvalidParameterError("ij must have shape (q, 2)")
+    if arr.numel():
+        lo = arr.min(dim=0).values.tolist()
+        hi = arr.max(dim=0).values.tolist()
+        if lo[0] < 0 or lo[1] < 0 or hi[0] >= sketch.n_rows or hi[1] >= sketch.n_cols:
+            raise InvalidParameterError(f"entries outside {sketch.n_rows} x {sketch.n_cols}")
+    p = sketch.params
+    polys = sketch.polys_device(device)
+    est, reps = _device.query(polys, sketch.words, p.d, p.log2b, p.transform, sketch.n_rows, sketch.n_cols, arr,
+                              want_reps=with_estimates)
+    if as_numpy:
+        est = est.cpu().numpy()
+        reps = reps.cpu().numpy() if reps is not None else None
+    return (est, reps) if with_estimates else est
+
+
 def decompress_rows(sketch: ProductSketch, r0: int = 0, r1: int | None = None, *, device=None, out=None):
     """Estimates of output rows [r0, r1) as a CUDA tensor (the row-sharded unit)."""
     from . import _device

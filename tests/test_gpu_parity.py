@@ -359,3 +359,22 @@ def test_two_pass_fft_against_oracle(log2b, n1, m, n2, d):
     polys = _device.finalize(acc, d, log2b, "fft").cpu().numpy()
     ref = O.compress(a, bm, b=1 << log2b, d=d, words=words, transform="fft", seed=0, threads=8)
     assert np.abs(polys - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_batched_entry_queries_match_scalar_path(name):
+    # per-entry queries on the device-resident sketch
+    w = W.make(name, xp=torch, device="cuda")
+    p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+    sk = P.compress(w.a, w.bmat, p)
+    rng = np.random.default_rng(3)
+    ij = rng.integers(0, w.n, size=(500, 2))
+    est, reps = P.decompress_entries(sk, ij, with_estimates=True)
+    for q in range(0, 500, 25):
+        i, j = int(ij[q, 0]), int(ij[q, 1])
+        assert np.array_equal(reps[q], P.sketch_estimates(sk, i, j))
+        assert est[q] == P.decompress_entry(sk, i, j)
+    full = P.decompress_rows(sk).cpu().numpy()
+    assert np.array_equal(est, full[ij[:, 0], ij[:, 1]])
+    with pytest.raises(P.InvalidParameterError):
+        P.decompress_entries(sk, [[0, w.n]])
