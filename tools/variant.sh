@@ -10,7 +10,7 @@ mkdir -p build/var_$NAME
 cp "$SRC" paper_2601_09477_b200/csrc/_variant_fwht2p.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -cudart static \
   --expt-relaxed-constexpr -Xptxas -v -dc -o build/var_$NAME/fwht2p.o paper_2601_09477_b200/csrc/_variant_fwht2p.cu \
-  2> build/var_$NAME/ptxas.log
+  2> build/var_$NAME/ptxas.log || { grep -i error build/var_$NAME/ptxas.log; rm -f paper_2601_09477_b200/csrc/_variant_fwht2p.cu; exit 1; }
 rm paper_2601_09477_b200/csrc/_variant_fwht2p.cu
 OBJS=$(ls build/smm/*.o | grep -v fwht2p.o)
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o paper_2601_09477_b200/_smm_b200_$NAME.so $OBJS build/var_$NAME/fwht2p.o
