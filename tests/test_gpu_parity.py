@@ -378,3 +378,22 @@ def test_batched_entry_queries_match_scalar_path(name):
     assert np.array_equal(est, full[ij[:, 0], ij[:, 1]])
     with pytest.raises(P.InvalidParameterError):
         P.decompress_entries(sk, [[0, w.n]])
+
+
+@pytest.mark.parametrize("transform,log2b", [("fwht", 10), ("fwht", 17), ("fft", 10), ("fft", 15)])
+def test_degenerate_hashes_everything_in_one_bucket(transform, log2b):
+    # a = 0 maps every key to bucket c >> shift: one bucket holds all n inputs (the
+    # gather loops' overflow paths, long CSR rows), against the oracle
+    n, m = 300, 40
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((n, m))
+    bm = rng.standard_normal((m, n))
+    d = 3
+    words = O.draw_words(5, d, 1 << log2b).copy()
+    words[0:2 * d:2] = 0          # h1: a = 0
+    words[2 * d:4 * d:2] = 0      # h2: a = 0
+    acc = _device.compress_accumulate(torch.from_numpy(a).cuda(), torch.from_numpy(bm).cuda(), words, d, log2b,
+                                      transform, 0, m, a_layout=_device.KMINOR, b_layout=_device.KMAJOR)
+    polys = _device.finalize(acc, d, log2b, transform).cpu().numpy()
+    ref = O.compress(a, bm, b=1 << log2b, d=d, words=words, transform=transform, seed=0, threads=8)
+    assert np.abs(polys - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
