@@ -224,6 +224,16 @@ def config_golden(name: str, threads: int = 8, full_polys: bool = False, sample:
     print(f"{name}: compress {tc:.1f}s decompress {td:.1f}s hh={hh.shape[0]} total {time.time() - t0:.1f}s", flush=True)
 
 
+def matrix_files():
+    """Matrix files written by the reference's matio (cli.py multiply's I/O)."""
+    from sketchmm import matio
+
+    m = np.array([[1.0, -2.5, 3.0e-300, 0.1], [np.pi, -0.0, 1e300, 7.0], [2.0 ** -1074, 5.0, -6.0, 1.0 / 3.0]])
+    matio.save_matrix_binary(OUT / "matrix_ref.dmat", m)
+    matio.save_matrix_csv(OUT / "matrix_ref.csv", m)
+    np.save(OUT / "matrix_ref.npy", m)
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     OUT.mkdir(parents=True, exist_ok=True)
@@ -246,6 +256,8 @@ def main():
                 for b in W.CFG5_B[:3]:
                     for d in W.CFG5_D:
                         config_golden(W.cfg5_name(b, d, nnz, transform), full_polys=(b <= 1 << 14 and nnz == 512))
+    if what in ("matrix", "all"):
+        matrix_files()
     if what == "cfg5big":
         for transform in ("fwht", "fft"):
             for b in W.CFG5_B[3:]:
