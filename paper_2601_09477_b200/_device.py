@@ -160,6 +160,21 @@ def stream_chunk(m: int, n_max: int) -> int:
     return max(32, min(kc, -(-m // 32) * 32))
 
 
+def _slab_bounds(m: int, kc: int) -> list:
+    """k-slabs of width kc, the last one split into kc/2, kc/4, kc/4 (multiples of 32):
+    uploads outpace nothing, so after the final upload only the last slab's compute
+    remains exposed — keep it small."""
+    bounds = [(c0, min(m, c0 + kc)) for c0 in range(0, m, kc)]
+    c0, c1 = bounds[-1]
+    w = c1 - c0
+    if len(bounds) > 1 and w >= 128:
+        h = ((w // 2 + 31) // 32) * 32
+        q = ((w // 4 + 31) // 32) * 32
+        cuts = [c0, c0 + h, min(c1, c0 + h + q), c1]
+        bounds = bounds[:-1] + [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    return bounds
+
+
 def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str,
                   a_layout: int, device: torch.device, chunk: int | None = None) -> torch.Tensor:
     """Pre-inverse accumulator of host-resident operands, streamed in k-slabs.
@@ -187,7 +202,7 @@ def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, l
     bbuf = [torch.empty((kc, n2), dtype=torch.float64, device=device) for _ in range(2)]
     loaded = [torch.cuda.Event() for _ in range(2)]
     freed = [torch.cuda.Event() for _ in range(2)]
-    slabs = [(c0, min(m, c0 + kc)) for c0 in range(0, m, kc)]
+    slabs = _slab_bounds(m, kc)
 
     def upload(c):
         c0, c1 = slabs[c]
