@@ -7,6 +7,7 @@ integer-valued, so its sketch must be bit-identical to the reference.
 """
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -76,9 +77,8 @@ def test_hash_tables_match_oracle_on_config_sizes():
         assert np.array_equal(_device.hash_table(h, 3, n).cpu().numpy().astype(np.float64), s2)
 
 
-CONFIGS = ["cfg1", "cfg2", "cfg3", "cfg5_b12_d3_nnz512_fwht", "cfg5_b12_d9_nnz512_fft", "cfg5_b14_d5_nnz512_fwht",
-           "cfg5_b14_d3_nnz512_fft", "cfg5_b16_d9_nnz512_fwht", "cfg5_b16_d5_nnz512_fft",
-           "cfg5_b18_d3_nnz512_fwht", "cfg5_b18_d3_nnz512_fft", "cfg5_b20_d3_nnz512_fwht", "cfg5_b20_d3_nnz512_fft"]
+# every BASELINE point with a reference golden (tools/make_golden.py): cfg1-3 and the cfg5 sweep
+CONFIGS = ["cfg1", "cfg2", "cfg3"] + sorted(p.stem for p in (Path(__file__).parent / "golden").glob("cfg5_*.npz"))
 
 
 @pytest.mark.parametrize("name", CONFIGS)
