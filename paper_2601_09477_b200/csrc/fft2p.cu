@@ -615,14 +615,21 @@ static Geom geometry(int log2b) {
   return g;
 }
 
-// units in flight: about 4 items per SM (2 CTAs x 2) must be dispensable, and a
-// group dispenses G1 + G2; the T ring ((lag + 2) slots) stays within ~64 MB of L2
-static int lag_for(const Geom &g) {
+// Ring plan (as fwht2p.cu): lag for ~4 dispensable items per SM, slack up to 6 units
+// between pass 2 and the pass-1 items that reuse its slots (pass-2 pair items weigh
+// about two pass-1 items; at slack 2, 45 % of CTA time went into pass-1 slot waits),
+// the T ring within ~96 MB of L2.
+static void ring_plan(const Geom &g, int &lag, int &nslot) {
   const int grp = g.G1 + g.G2;
-  int lag = (4 * num_sms() + grp - 1) / grp;
-  const int cap = (int)(((int64_t)64 << 20) / (g.halves * g.bs * KT * 16)) - 2;
-  if (lag > cap) lag = cap;
-  return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+  const int64_t slot = (int64_t)g.halves * g.bs * KT * 16;
+  int maxslots = (int)(((int64_t)96 << 20) / slot);
+  if (maxslots < 3) maxslots = 3;
+  lag = (4 * num_sms() + grp - 1) / grp;
+  if (lag > maxslots - 2) lag = maxslots - 2;
+  lag = lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+  int slack = maxslots - lag;
+  slack = slack < 2 ? 2 : (slack > 6 ? 6 : slack);
+  nslot = lag + slack;
 }
 }  // namespace f2p
 
@@ -638,7 +645,9 @@ int64_t fft2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   w += pad256((int64_t)d * 2 * g.bs * 4);                      // cnt / fill
   w += pad256((int64_t)d * 2 * nmax * 4);                      // ent
   w += pad256(b * 16);                                         // twiddles w_b^x
-  w += pad256((int64_t)(f2p::lag_for(g) + 2) * g.halves * g.bs * f2p::KT * 16);  // T ring
+  int lag, nslot;
+  f2p::ring_plan(g, lag, nslot);
+  w += pad256((int64_t)nslot * g.halves * g.bs * f2p::KT * 16);  // T ring
   w += pad256((1 + 2 * U + (int64_t)d * g.NPU * g.G2) * 4);    // counters
   return w;
 }
@@ -672,8 +681,8 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   double *twb = (double *)q;
   q += pad256(b * 16);
   double *Y = (double *)q;
-  const int lag = lag_for(g);
-  const int nslot = lag + 2;
+  int lag, nslot;
+  ring_plan(g, lag, nslot);
   q += pad256((int64_t)nslot * g.halves * bs * KT * 16);
   int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;

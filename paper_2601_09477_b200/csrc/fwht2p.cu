@@ -33,7 +33,7 @@ namespace smm {
 constexpr int P_THREADS = 256;
 constexpr int KT = 32;
 constexpr int P1_BITS = 8;
-// P2(u) is dispensed `lag` groups after P1(u) (lag_for(): 1 at b = 2^16, where 2 was
+// P2(u) is dispensed `lag` groups after P1(u) (ring_plan(): 1 at b = 2^16, where 2 was
 // measured slower; small transforms have few items per unit and need more units in flight)
 
 // Optional phase profiler (env SMM_PROFILE=1): thread 0 of every CTA accumulates
@@ -656,16 +656,22 @@ bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
   return faster && log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
-// units in flight: ~2 CTAs per SM need about 2 * num_sms items; a unit dispenses 2 * nblk
-// units in flight: about 4 items per SM (2 CTAs x 2) must be dispensable, and a
-// group dispenses 2 * nblk; the Y ring ((lag + 2) slots) stays within ~64 MB of L2
-static int lag_for(int LB) {
+// Ring plan.  lag: units between a unit's pass 1 and its pass 2, so that about 4
+// items per SM are dispensable (a group dispenses 2 * nblk).  nslot = lag + slack:
+// pass 1 of unit u reuses the Y slot of pass 2 of unit u - nslot, so the slack is
+// how far pass 2 may trail before a pass-1 item has to wait (fft2p measured 45 % of
+// CTA time in such waits at slack 2).  The ring stays within ~96 MB of the L2.
+static void ring_plan(int LB, int &lag, int &nslot) {
   const int nblk = 1 << (LB - P1_BITS);
   const int64_t slot = (int64_t)2 * (1 << LB) * KT * 8;
-  int lag = (4 * num_sms() + 2 * nblk - 1) / (2 * nblk);
-  const int cap = (int)(((int64_t)64 << 20) / slot) - 2;
-  if (lag > cap) lag = cap;
-  return lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+  int maxslots = (int)(((int64_t)96 << 20) / slot);
+  if (maxslots < 3) maxslots = 3;
+  lag = (4 * num_sms() + 2 * nblk - 1) / (2 * nblk);
+  if (lag > maxslots - 2) lag = maxslots - 2;
+  lag = lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+  int slack = maxslots - lag;
+  slack = slack < 2 ? 2 : (slack > 6 ? 6 : slack);
+  nslot = lag + slack;
 }
 
 // geometry: LB-bit slices, F = 2^(log2b - LB) of them (the fold of DESIGN.md §5)
@@ -686,7 +692,9 @@ int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   w += pad256((int64_t)d * 2 * (bs + 1) * 4);  // off
   w += pad256((int64_t)d * 2 * bs * 4);        // cnt / fill
   w += pad256((int64_t)d * 2 * nmax * 4);      // ent
-  w += pad256((int64_t)(lag_for(LB) + 2) * 2 * bs * KT * 8);  // Y ring
+  int lag, nslot;
+  ring_plan(LB, lag, nslot);
+  w += pad256((int64_t)nslot * 2 * bs * KT * 8);  // Y ring
   w += pad256((1 + 2 * U + (int64_t)d * F * nblk) * 4);       // counters
   return w;
 }
@@ -717,8 +725,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   uint32_t *ent = (uint32_t *)q;
   q += pad256((int64_t)d * 2 * nmax * 4);
   double *Y = (double *)q;
-  const int lag = lag_for(LB);
-  const int nslot = lag + 2;
+  int lag, nslot;
+  ring_plan(LB, lag, nslot);
   q += pad256((int64_t)nslot * 2 * bs * KT * 8);
   int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;

@@ -112,8 +112,25 @@ __global__ void cscale_kernel(cplx *z, int64_t n, double scale) {
   }
 }
 
+// The stream-ordered scratch below comes from the device's default memory pool;
+// with its default release threshold (0) every synchronisation returns the memory
+// to the driver and the next cudaMallocAsync maps it again (milliseconds of host
+// time while the GPU idles).  Keep freed blocks in the pool.
+static void keep_pool_memory() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 int fft_batched(cplx *z, int64_t batch, int log2n, int inverse, double scale, cudaStream_t s) {
   if (batch <= 0) return SMM_OK;
+  keep_pool_memory();
   const int64_t n = (int64_t)1 << log2n;
   cplx *tab = nullptr;
   SMM_CUDA_TRY(cudaMallocAsync((void **)&tab, twiddle_table_bytes(log2n) + 16, s), "fft twiddle alloc");
@@ -190,6 +207,7 @@ int finalize(int variant, const void *acc, double *polys, int d, int log2b, cuda
     return fwht_batched(polys, d, log2b, inv, s);
   }
   cplx *z = nullptr;
+  keep_pool_memory();
   SMM_CUDA_TRY(cudaMallocAsync((void **)&z, (size_t)d * b * sizeof(cplx), s), "finalize alloc");
   hermitian_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>((const cplx *)acc, z, d, log2b);
   SMM_LAUNCH_CHECK("hermitian_fill_kernel");
