@@ -377,8 +377,8 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
 }
 
 __device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double *S,
+                                        const PullHead &hd1,
                                         const PullHead &hd0) {
-  const PullHead hd1 = pull_head(p, t, 1, blk);  // operand 1's head lands while operand 0 computes
   double xpre[8];
   p1_operand(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
   __syncthreads();  // every warp has read operand 0's exchange data from S
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  PullHead hd_next;
+  PullHead hd_next, hd_next1;  // both operands' CSR heads of the next pass-1 item
   bool hd_valid = false;
   while (true) {
     if (tid == 0) {
@@ -614,11 +614,17 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
     }
     if (!go) break;
-    PullHead hd_cur;
-    if (is_p1) hd_cur = hd_valid ? hd_next : pull_head(p, t, 0, idx);
+    PullHead hd_cur, hd_cur1;
+    if (is_p1) {
+      hd_cur = hd_valid ? hd_next : pull_head(p, t, 0, idx);
+      hd_cur1 = hd_valid ? hd_next1 : pull_head(p, t, 1, idx);
+    }
     hd_valid = next_p1 != 0;
-    if (hd_valid) hd_next = pull_head(p, next_t, 0, next_idx);  // lands while this item computes
-    if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur);
+    if (hd_valid) {  // land while this item computes
+      hd_next = pull_head(p, next_t, 0, next_idx);
+      hd_next1 = pull_head(p, next_t, 1, next_idx);
+    }
+    if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
     else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_cnt + (t * p.F + asl) * p.nblk + idx, S);
     tc_fence_before();
     PROF_MARK(2);
