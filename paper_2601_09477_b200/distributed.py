@@ -77,6 +77,36 @@ def reduce_accumulator(acc, group=None, all_reduce=None):
     return acc
 
 
+def gather_heavy_hitters(pairs, dst: int = 0, group=None):
+    """Collect the row-sharded heavy-hitter lists on rank ``dst``.
+
+    Rank g extracted output rows [g n/G, (g+1) n/G), so its pairs are already in
+    row-major order and concatenating the ranks' lists in rank order is the
+    global row-major list.  One all_gather of the counts, one of the lists padded
+    to the largest count (all_gather works on every backend, gather does not).
+    Returns the (k, 2) int64 tensor on ``dst`` and None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return pairs
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    pairs = pairs.to(torch.int64).reshape(-1, 2)
+    cnt = torch.tensor([pairs.shape[0]], dtype=torch.int64, device=pairs.device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    padded = torch.zeros((max(counts), 2), dtype=torch.int64, device=pairs.device)
+    padded[:pairs.shape[0]] = pairs
+    bufs = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(bufs, padded, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([buf[:c] for buf, c in zip(bufs, counts)])
+
+
 def plan_shards(m: int, n_rows: int, world: int) -> list[dict]:
     """Host-side description of every rank's k-slab and output-row block."""
     out = []

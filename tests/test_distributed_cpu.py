@@ -50,7 +50,15 @@ def _worker(rank, world, port, q):
         r0, r1 = D.row_bounds(n, world, rank)
         est, _, _ = O.decompress(polys, words, b=b, d=d, transform="fwht", n1=n, n2=n, r0=r0, r1=r1)
         est_ref, _, _ = O.decompress(ref, words, b=b, d=d, transform="fwht", n1=n, n2=n)
-        q.put((rank, bool(np.array_equal(polys, ref)), bool(np.array_equal(est, est_ref[r0:r1]))))
+        # heavy hitters: each rank thresholds its own rows, rank 0 collects the global list
+        thr = float(np.quantile(np.abs(est_ref), 0.9))
+        ii, jj = np.nonzero(np.abs(est) > thr)
+        local = torch.from_numpy(np.stack([ii + r0, jj], axis=1).astype(np.int64))
+        got = D.gather_heavy_hitters(local)
+        gi, gj = np.nonzero(np.abs(est_ref) > thr)
+        want = np.stack([gi, gj], axis=1)
+        hh_ok = (got is None) if rank else bool(np.array_equal(got.numpy(), want))
+        q.put((rank, bool(np.array_equal(polys, ref)), bool(np.array_equal(est, est_ref[r0:r1])) and hh_ok))
     finally:
         dist.destroy_process_group()
 
