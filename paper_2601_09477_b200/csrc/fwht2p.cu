@@ -409,6 +409,77 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   const uint32_t col_fa = (uint32_t)(wh * 64);
   double v[32];
   const uint64_t pol = policy_evict_first();
+  if constexpr (HB > 5) {
+    // Operand 0 goes through the shared-memory exchange and into TMEM in chunks of
+    // 8 registers, so operand 1's 32 row loads can already fly during that half.
+    const double *Y0 = p.Y + ((int64_t)slot * 2 + 0) * p.bsz * KT + lane;
+    const double *Y1 = p.Y + ((int64_t)slot * 2 + 1) * p.bsz * KT + lane;
+    auto load = [&](const double *Ys) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int sg = r | (warp << 5);
+        v[r] = ld_hint(Ys + ((int64_t)(sg & hmask) * 256 + lo0 + (sg >> hb)) * KT, pol);
+      }
+    };
+    auto discard = [&](const double *Ys) {  // last use of these Y rows: drop them without write-back
+      __syncwarp();
+      const int sg = lane | (warp << 5);
+      const double *row = Ys - lane + ((int64_t)(sg & hmask) * 256 + lo0 + (sg >> hb)) * KT;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(row) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + 16) : "memory");
+    };
+    load(Y0);
+    PROF_MARK(8);
+    reg_fwht32(v, 0, 5);
+    discard(Y0);
+    // exchange: warp bits (sigma 5-7) <-> register bits 2-4
+#pragma unroll
+    for (int r = 0; r < 32; ++r) S[(warp * 32 + r) * 32 + lane] = v[r];
+    load(Y1);
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // registers c + 4 j: the remaining stages run over register bits 2-4 = j bits 0-2
+      double f[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = c + 4 * j;
+        f[j] = S[((r >> 2) * 32 + ((r & 3) | (warp << 2))) * 32 + lane];
+      }
+#pragma unroll
+      for (int q = 0; q < hb - 5; ++q) {
+        const int h = 1 << q;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (!(j & h)) {
+            const double x = f[j], y = f[j + h];
+            f[j] = x + y;
+            f[j + h] = x - y;
+          }
+      }
+      tmem_st8(tq + col_fa + 16 * c, f);
+    }
+    tmem_wait_st();
+    __syncthreads();  // S is reused by operand 1's exchange
+    reg_fwht32(v, 0, 5);
+    discard(Y1);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) S[(warp * 32 + r) * 32 + lane] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = S[((r >> 2) * 32 + ((r & 3) | (warp << 2))) * 32 + lane];
+    reg_fwht32(v, 2, 2 + (hb - 5));
+    __syncthreads();  // S is reused by the reduction
+    PROF_MARK(9);
+    // product FA * FB: TMEM chunk c holds FA of registers c + 4 j
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double fa[8];
+      tmem_ld8(tq + col_fa + 16 * c, fa);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[c + 4 * j] *= fa[j];
+    }
+  } else {
 #pragma unroll 1
   for (int op = 0; op < 2; ++op) {
     const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + lane;
@@ -452,6 +523,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
     tmem_ld8(tq + col_fa + 16 * c, fa);
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
+  }
   }
   // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory:
   // lane l ends with register l summed over all lanes, in lane order
