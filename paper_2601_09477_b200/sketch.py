@@ -4,9 +4,10 @@ Same names, argument meaning, validation and exceptions as the reference
 (sketch.py:58-494, exported at __init__.py:9-75).  The difference is where the
 work runs: hashing tables, compression (steps 1-3), the inverse transform
 (step 4) and extraction + heavy-hitter threshold (step 5) all execute in the
-sm_100a kernels of ``_smm_b200.so``; inputs may be numpy arrays (copied to the
-GPU) or torch tensors (used in place when already float64 on CUDA).  There is
-no CPU fallback: without the extension or a GPU every hot-path call raises.
+sm_100a kernels of ``_smm_b200.so``; inputs may be host arrays (numpy or CPU
+tensors: streamed to the GPU in k-slabs that overlap the kernel) or CUDA
+tensors (used in place when float64).  There is no CPU fallback: without the
+extension or a GPU every hot-path call raises.
 
 Reference behaviour kept on purpose:
   * validation happens before any kernel work (sketch.py:68-82, 266-301, 335-355);

@@ -258,6 +258,14 @@ def main():
                         config_golden(W.cfg5_name(b, d, nnz, transform), full_polys=(b <= 1 << 14 and nnz == 512))
     if what in ("matrix", "all"):
         matrix_files()
+    if what == "cfg5rest":  # every remaining cfg5 point (b = 2^18, 2^20), skipping existing fixtures
+        for b in W.CFG5_B[3:]:
+            for d in W.CFG5_D:
+                for nnz in W.CFG5_NNZ:
+                    for transform in ("fwht", "fft"):
+                        name = W.cfg5_name(b, d, nnz, transform)
+                        if not (OUT / f"{name}.npz").exists():
+                            config_golden(name)
     if what == "cfg5big":
         for transform in ("fwht", "fft"):
             for b in W.CFG5_B[3:]:
