@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "plan.cuh"
+#include "twopass.cuh"
 
 namespace smm {
 
@@ -469,7 +470,6 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
 #pragma unroll
     for (int r = 0; r < 32; ++r) v[r] = S[((r >> 2) * 32 + ((r & 3) | (warp << 2))) * 32 + lane];
     reg_fwht32(v, 2, 2 + (hb - 5));
-    __syncthreads();  // S is reused by the reduction
     PROF_MARK(9);
     // product FA * FB: TMEM chunk c holds FA of registers c + 4 j
 #pragma unroll
@@ -507,7 +507,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = S[((r >> 2) * 32 + ((r & 3) | (warp << 2))) * 32 + lane];
       reg_fwht32(v, 2, 2 + (hb - 5));
-      __syncthreads();  // S is reused by the next exchange / the reduction
+      __syncthreads();  // S is reused by the next exchange
     }
     if (op == 0) {
 #pragma unroll
@@ -525,15 +525,8 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
     for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
   }
   }
-  // sum over the 32 inner indices (lanes) through this warp's 8 KB of shared memory:
-  // lane l ends with register l summed over all lanes, in lane order
-  double *W = S + warp * 1024;
-#pragma unroll
-  for (int r = 0; r < 32; ++r) W[r * 32 + (lane ^ r)] = v[r];
-  __syncwarp();
-  double sum = 0.0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) sum += W[lane * 32 + (j ^ lane)];
+  // sum over the 32 inner indices (lanes): lane l ends with register l summed over all lanes
+  const double sum = tp::lane_sum32(v, lane);
   if (kappa == 0) {
     // accumulate mode continues a previous call's k order exactly (chunk boundaries are k-tiles)
     __stcg(a, p.acc_add ? acc_old + sum : sum);

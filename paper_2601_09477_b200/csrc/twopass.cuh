@@ -93,5 +93,28 @@ static __device__ __forceinline__ void ld2_hint(const double *p, double &a, doub
                : "memory");
 }
 
+// Sum over the 32 lanes of a warp, for each of 32 registers: recursive halving
+// through shuffles (31 double shuffles per lane, no shared memory).  Lane l ends
+// with register l summed over all lanes.
+template <int H>
+static __device__ __forceinline__ void halve_step(double (&v)[32], int lane) {
+  const bool hi = (lane & H) != 0;
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    const double send = hi ? v[r] : v[r + H];
+    const double keep = hi ? v[r + H] : v[r];
+    v[r] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+  }
+}
+
+static __device__ __forceinline__ double lane_sum32(double (&v)[32], int lane) {
+  halve_step<16>(v, lane);
+  halve_step<8>(v, lane);
+  halve_step<4>(v, lane);
+  halve_step<2>(v, lane);
+  halve_step<1>(v, lane);
+  return v[0];
+}
+
 }  // namespace tp
 }  // namespace smm
