@@ -619,17 +619,18 @@ static Geom geometry(int log2b) {
 // between pass 2 and the pass-1 items that reuse its slots (pass-2 pair items weigh
 // about two pass-1 items; at slack 2, 45 % of CTA time went into pass-1 slot waits),
 // the T ring within ~96 MB of L2.
-static void ring_plan(const Geom &g, int &lag, int &nslot) {
+static void ring_plan(const Geom &g, int64_t U, int &lag, int &nslot) {
   const int grp = g.G1 + g.G2;
   const int64_t slot = (int64_t)g.halves * g.bs * KT * 16;
   int maxslots = (int)(((int64_t)96 << 20) / slot);
   if (maxslots < 3) maxslots = 3;
   lag = (4 * num_sms() + grp - 1) / grp;
   if (lag > maxslots - 2) lag = maxslots - 2;
-  lag = lag < 1 ? 1 : (lag > 8 ? 8 : lag);
-  int slack = maxslots - lag;
-  slack = slack < 2 ? 2 : (slack > 6 ? 6 : slack);
+  lag = lag < 1 ? 1 : (lag > 64 ? 64 : lag);
+  int slack = maxslots - lag;  // whatever the L2 budget leaves (cfg5 b = 2^12: 4.2 -> 3.6 ms)
+  slack = slack < 2 ? 2 : slack;
   nslot = lag + slack;
+  if (nslot > U + 1) nslot = (int)(U + 1 > lag + 1 ? U + 1 : lag + 1);
 }
 }  // namespace f2p
 
@@ -646,7 +647,7 @@ int64_t fft2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   w += pad256((int64_t)d * 2 * nmax * 4);                      // ent
   w += pad256(b * 16);                                         // twiddles w_b^x
   int lag, nslot;
-  f2p::ring_plan(g, lag, nslot);
+  f2p::ring_plan(g, U, lag, nslot);
   w += pad256((int64_t)nslot * g.halves * g.bs * f2p::KT * 16);  // T ring
   w += pad256((1 + 2 * U + (int64_t)d * g.NPU * g.G2) * 4);    // counters
   return w;
@@ -681,12 +682,12 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   double *twb = (double *)q;
   q += pad256(b * 16);
   double *Y = (double *)q;
-  int lag, nslot;
-  ring_plan(g, lag, nslot);
-  q += pad256((int64_t)nslot * g.halves * bs * KT * 16);
-  int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;
   const int64_t U = ntiles * d * g.NPU;
+  int lag, nslot;
+  ring_plan(g, U, lag, nslot);
+  q += pad256((int64_t)nslot * g.halves * bs * KT * 16);
+  int *ctr = (int *)q;
   const int N2 = g.N2, G1 = g.G1, G2 = g.G2;
   const size_t acc_bytes = (size_t)d * (size_t)(b / 2 + 1) * 16;
   if (K <= 0) {

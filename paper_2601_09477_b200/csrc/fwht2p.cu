@@ -260,7 +260,7 @@ __device__ __forceinline__ void reg_fwht32(double (&v)[32], int qlo, int qhi) {
 // Pass 1: pull the 256 buckets [blk*256, blk*256+256) of operand op for the
 // 32 inner indices of k-tile kappa, FWHT over the 8 low bucket bits, write Y.
 // Warp w owns buckets blk*256 + w*32 + j (j = register index), lanes = k.
-// CSR range of one warp's 32 buckets and its first 8 entries, fetched ahead of use
+// CSR range of one warp's 32 buckets and its first 32 entry words (one per lane), fetched ahead of use
 struct PullHead {
   int e_lo, e_hi;
   uint32_t first;
@@ -274,7 +274,7 @@ __device__ __forceinline__ PullHead pull_head(const TwoPassArgs &p, int t, int o
   PullHead h;
   h.e_lo = __ldg(off + base);
   h.e_hi = __ldg(off + base + 32);
-  h.first = (lane < 8 && h.e_lo + lane < h.e_hi) ? __ldg(p.ent + row * p.nmax + h.e_lo + lane) : 0u;
+  h.first = h.e_lo + lane < h.e_hi ? __ldg(p.ent + row * p.nmax + h.e_lo + lane) : 0u;
   return h;
 }
 
@@ -314,13 +314,17 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
   double *col = S + warp * 1024 + lane;
   uint32_t mask = 0;  // buckets with an entry (warp-uniform)
   int prevj = -1;
+  uint32_t win = hd.first;  // entry words [wbase, wbase + 32), one per lane
+  int wbase = e_lo;
   for (int eb = e_lo; eb < e_hi; eb += 8) {
-    const uint32_t mine =
-        eb == e_lo ? hd.first : ((lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u);
+    if (eb - wbase == 32) {
+      wbase = eb;
+      win = eb + lane < e_hi ? __ldg(ent + eb + lane) : 0u;
+    }
     uint32_t es[8];
     double x[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
+    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, win, (eb - wbase) + s);
     if (have_pre && eb == e_lo) {
 #pragma unroll
       for (int s = 0; s < 8; ++s) x[s] = xpre[s];
@@ -723,26 +727,29 @@ constexpr int MAX_LB = 16;  // per-slice transform bits handled by the two passe
 // n=8192: 4.2 ms vs 7.3 ms); from b = 2^16 on the two-pass kernel always wins.
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
   const int64_t nmax = n1 > n2 ? n1 : n2;
-  const bool faster = log2b >= 16 || ((int64_t)1 << log2b) >= nmax;
-  return faster && log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
+  (void)nmax;
+  return log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 
 // Ring plan.  lag: units between a unit's pass 1 and its pass 2, so that about 4
 // items per SM are dispensable (a group dispenses 2 * nblk).  nslot = lag + slack:
 // pass 1 of unit u reuses the Y slot of pass 2 of unit u - nslot, so the slack is
-// how far pass 2 may trail before a pass-1 item has to wait (fft2p measured 45 % of
-// CTA time in such waits at slack 2).  The ring stays within ~96 MB of the L2.
-static void ring_plan(int LB, int &lag, int &nslot) {
+// how far pass 2 may trail before a pass-1 item has to wait; it takes whatever the
+// ~96 MB L2 budget leaves (small transforms: 2 MB slots at b = 2^12, where slack 6
+// measured 3.7 ms and slack 29 2.4 ms on cfg5 b = 2^12, d = 3).  At most U + 1
+// slots are ever used.
+static void ring_plan(int LB, int64_t U, int &lag, int &nslot) {
   const int nblk = 1 << (LB - P1_BITS);
   const int64_t slot = (int64_t)2 * (1 << LB) * KT * 8;
   int maxslots = (int)(((int64_t)96 << 20) / slot);
   if (maxslots < 3) maxslots = 3;
   lag = (4 * num_sms() + 2 * nblk - 1) / (2 * nblk);
   if (lag > maxslots - 2) lag = maxslots - 2;
-  lag = lag < 1 ? 1 : (lag > 8 ? 8 : lag);
+  lag = lag < 1 ? 1 : (lag > 64 ? 64 : lag);
   int slack = maxslots - lag;
-  slack = slack < 2 ? 2 : (slack > 6 ? 6 : slack);
+  slack = slack < 2 ? 2 : slack;
   nslot = lag + slack;
+  if (nslot > U + 1) nslot = (int)(U + 1 > lag + 1 ? U + 1 : lag + 1);
 }
 
 // geometry: LB-bit slices, F = 2^(log2b - LB) of them (the fold of DESIGN.md §5)
@@ -764,7 +771,7 @@ int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   w += pad256((int64_t)d * 2 * bs * 4);        // cnt / fill
   w += pad256((int64_t)d * 2 * nmax * 4);      // ent
   int lag, nslot;
-  ring_plan(LB, lag, nslot);
+  ring_plan(LB, U, lag, nslot);
   w += pad256((int64_t)nslot * 2 * bs * KT * 8);  // Y ring
   w += pad256((1 + 2 * U + (int64_t)d * F * nblk) * 4);       // counters
   return w;
@@ -796,12 +803,12 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   uint32_t *ent = (uint32_t *)q;
   q += pad256((int64_t)d * 2 * nmax * 4);
   double *Y = (double *)q;
-  int lag, nslot;
-  ring_plan(LB, lag, nslot);
-  q += pad256((int64_t)nslot * 2 * bs * KT * 8);
-  int *ctr = (int *)q;
   const int64_t ntiles = (K + KT - 1) / KT;
   const int64_t U = ntiles * d * F;
+  int lag, nslot;
+  ring_plan(LB, U, lag, nslot);
+  q += pad256((int64_t)nslot * 2 * bs * KT * 8);
+  int *ctr = (int *)q;
   const int nblk = (int)(bs >> P1_BITS);
   if (K <= 0) {
     if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
