@@ -7,6 +7,7 @@ CPU oracle (the bit-exact port of the reference algorithm, all host threads) on
 a bounded k-slice / row-slice of the same instance, extrapolated.
 
     python tools/config_bench.py [cfg ...]  ->  profiles/r01_configs.{json,md}
+    python tools/config_bench.py --from-log LOG   (tables from a run's printed JSON lines)
 """
 import json
 import sys
@@ -97,6 +98,10 @@ def main(names):
         print(json.dumps(row), flush=True)
         del w, sk
         torch.cuda.empty_cache()
+    write_tables(rows)
+
+
+def write_tables(rows):
     out = ROOT / "profiles" / "r01_configs.json"
     out.write_text(json.dumps(rows, indent=1))
     lines = ["| config | transform | n | b | d | compress ms | FP64 frac | extract ms | est. write GB/s | "
@@ -115,4 +120,7 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or DEFAULT)
+    if sys.argv[1:2] == ["--from-log"]:  # rebuild the tables from the JSON lines of a GPU-box run
+        write_tables([json.loads(ln) for ln in open(sys.argv[2]) if ln.startswith("{")])
+    else:
+        main(sys.argv[1:] or DEFAULT)
