@@ -361,6 +361,24 @@ def test_two_pass_fft_against_oracle(log2b, n1, m, n2, d):
     assert np.abs(polys - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("log2b,n1,m,n2,d", [(8, 3000, 70, 2000, 3), (10, 5000, 96, 4000, 5), (12, 9000, 45, 8000, 3),
+                                             (14, 1000, 1, 900, 9), (16, 700, 33, 650, 3), (17, 400, 31, 350, 3),
+                                             (20, 300, 37, 280, 3)])
+def test_two_pass_fwht_against_oracle(log2b, n1, m, n2, d):
+    # fwht2p across its whole range: dense pulls (n >> b: hundreds of CSR entries per warp,
+    # several 32-entry windows), a single inner index, partial k-tiles, the fold (b > 2^16),
+    # rectangular operands; against the oracle (reference algorithm) at 1e-12 relative
+    rng = np.random.default_rng(log2b + 7)
+    a = rng.standard_normal((n1, m))
+    bm = rng.standard_normal((m, n2))
+    words = O.draw_words(log2b + 200, d, 1 << log2b)
+    acc = _device.compress_accumulate(torch.from_numpy(a).cuda(), torch.from_numpy(bm).cuda(), words, d, log2b, "fwht",
+                                      0, m, a_layout=_device.KMINOR, b_layout=_device.KMAJOR)
+    polys = _device.finalize(acc, d, log2b, "fwht").cpu().numpy()
+    ref = O.compress(a, bm, b=1 << log2b, d=d, words=words, transform="fwht", seed=0, threads=8)
+    assert np.abs(polys - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
 def test_batched_entry_queries_match_scalar_path(name):
     # per-entry queries on the device-resident sketch
