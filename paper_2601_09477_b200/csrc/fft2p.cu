@@ -110,18 +110,37 @@ struct Args {
   int acc_add;
 };
 
+// CSR range of one warp's 16 tile positions of operand OP and its first 32 entry
+// words (one per lane), fetched ahead of the pull
+struct Head {
+  int e_lo, e_hi;
+  uint32_t win;
+};
+
+template <int OP>
+__device__ __forceinline__ Head head(const Args &p, int t, int item) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)t * 2 + OP;
+  const int32_t *off = p.off + row * (p.bsz + 1) + (int64_t)item * 128 + warp * 16;
+  Head h;
+  h.e_lo = __ldg(off);
+  h.e_hi = __ldg(off + 16);
+  h.win = h.e_lo + lane < h.e_hi ? __ldg(p.ent + row * p.nmax + h.e_lo + lane) : 0u;
+  return h;
+}
+
 // signed gather of one operand into the real (op 0) or imaginary (op 1) parts of the
 // warp's lane-private complex columns of the exchange area (S2[(16 w + j) * 32 + lane],
 // j = tile position & 15) — a register target would need a jump per entry.  Entries
 // are sorted by position: the first of a position stores, later ones add.  Returns the
 // mask of positions written.
 template <int OP, bool FOLD>
-__device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, int a, double *S, uint32_t &mask) {
+__device__ __forceinline__ void pull(const Args &p, int kappa, int t, const Head &hd, int a, double *S,
+                                     uint32_t &mask) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)t * 2 + OP;
-  const int32_t *off = p.off + row * (p.bsz + 1) + (int64_t)item * 128 + warp * 16;
   const uint32_t *ent = p.ent + row * p.nmax;
-  const int e_lo = __ldg(off), e_hi = __ldg(off + 16);
+  const int e_lo = hd.e_lo, e_hi = hd.e_hi;
   const int64_t kk = (int64_t)kappa * KT + lane;
   const char *Xb = (const char *)(p.X[OP] + p.k0 + (kk < p.K ? kk : p.K - 1));
   const uint32_t ldb = (uint32_t)(p.ld[OP] * 8);
@@ -129,12 +148,17 @@ __device__ __forceinline__ void pull(const Args &p, int kappa, int t, int item, 
   // both parts of its position; otherwise operand OP owns one part
   double *col = S + ((warp * 16) * 32 + lane) * 2 + (FOLD ? 0 : OP);
   const uint32_t bmask = (uint32_t)(p.bfull - 1);
+  uint32_t win = hd.win;  // entry words [wbase, wbase + 32)
+  int wbase = e_lo;
   for (int eb = e_lo; eb < e_hi; eb += 8) {
-    const uint32_t mine = (lane < 8 && eb + lane < e_hi) ? __ldg(ent + eb + lane) : 0u;
+    if (eb - wbase == 32) {
+      wbase = eb;
+      win = eb + lane < e_hi ? __ldg(ent + eb + lane) : 0u;
+    }
     uint32_t es[8];
     double x[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, mine, s);
+    for (int s = 0; s < 8; ++s) es[s] = __shfl_sync(0xffffffffu, win, (eb - wbase) + s);
 #pragma unroll
     for (int s = 0; s < 8; ++s)
       x[s] = eb + s < e_hi ? __ldg((const double *)(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb)) : 0.0;
@@ -254,13 +278,16 @@ __device__ __forceinline__ void p1_item(const Args &p, int kappa, int t, int pu,
     item = idx & 127;
     a = half ? (pu == 0 ? p.F / 2 : p.F - pu) : pu;  // unit 0 = the self-paired slices {0, F/2}
   }
+  // both operands' CSR heads up front: operand 1's land while operand 0 pulls
+  const Head h0 = head<0>(p, t, item);
+  const Head h1 = head<1>(p, t, item);
   uint32_t m0 = 0, m1 = 0;
-  pull<0, FOLD>(p, kappa, t, item, a, S, m0);
+  pull<0, FOLD>(p, kappa, t, h0, a, S, m0);
   if (FOLD) {
-    pull<1, true>(p, kappa, t, item, a, S, m0);
+    pull<1, true>(p, kappa, t, h1, a, S, m0);
     m1 = m0;
   } else {
-    pull<1, false>(p, kappa, t, item, a, S, m1);
+    pull<1, false>(p, kappa, t, h1, a, S, m1);
   }
   double v[32];
   {
