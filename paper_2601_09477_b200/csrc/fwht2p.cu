@@ -66,31 +66,44 @@ __global__ void csr_count_kernel(SketchHashes h, int64_t n1, int64_t n2, int32_t
   }
 }
 
+// exclusive scan of one (t, op) row of bucket counts per 1024-thread block: each
+// thread owns a contiguous chunk (sum, one block-wide scan of the chunk sums,
+// then the chunk's offsets) — two barriers instead of two per element batch
 __global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b) {
-  __shared__ int32_t s[1024];
-  __shared__ int32_t carry;
+  __shared__ int32_t wsum[32];
   const int64_t row = blockIdx.x;  // (t, op)
   const int32_t *c = cnt + row * b;
   int32_t *o = off + row * (b + 1);
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < b; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t v = i < b ? c[i] : 0;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int d = 1; d < 1024; d <<= 1) {
-      int32_t add = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
-      __syncthreads();
-      s[threadIdx.x] += add;
-      __syncthreads();
-    }
-    if (i < b) o[i] = carry + s[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += s[1023];
-    __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (b + 1023) / 1024;
+  const int64_t lo = threadIdx.x * per < b ? threadIdx.x * per : b;
+  const int64_t hi = lo + per < b ? lo + per : b;
+  int32_t sum = 0;
+  for (int64_t i = lo; i < hi; ++i) sum += c[i];
+  int32_t inc = sum;  // inclusive scan within the warp
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
   }
-  if (threadIdx.x == 0) o[b] = carry;
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int32_t run = inc - sum + (warp > 0 ? wsum[warp - 1] : 0);
+  for (int64_t i = lo; i < hi; ++i) {
+    o[i] = run;
+    run += c[i];
+  }
+  if (threadIdx.x == 1023) o[b] = wsum[31];
 }
 
 __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const int32_t *off, int32_t *fill,
@@ -609,11 +622,23 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   // right after the item's closing barrier, concurrently with thread 0's
   // scheduling, so the fence latency is not serialised with it.  Every warp
   // prefetches the CSR head of the next pass-1 item during the current item.
-  int64_t nxt = 0;
-  Item itn;
-  const int *dep_ptr = nullptr;
-  int dep_target = 0, dep_val = 0;
-  int ver1 = -1, ver2 = -1;  // highest unit whose P1 / P2 completion this CTA has seen
+  // scheduler state lives in shared memory: only thread 0 touches it, and as
+  // registers it would cost every thread ~14 of its 128
+  __shared__ int64_t sh_nxt;
+  __shared__ Item sh_itn;
+  __shared__ const int *sh_dep_ptr;
+  __shared__ int sh_dep_target, sh_dep_val, sh_ver1, sh_ver2;
+  int64_t &nxt = sh_nxt;
+  Item &itn = sh_itn;
+  const int *&dep_ptr = sh_dep_ptr;
+  int &dep_target = sh_dep_target, &dep_val = sh_dep_val;
+  int &ver1 = sh_ver1, &ver2 = sh_ver2;  // highest unit whose P1 / P2 completion this CTA has seen
+  if (tid == 0) {
+    nxt = 0;
+    dep_ptr = nullptr;
+    dep_target = dep_val = 0;
+    ver1 = ver2 = -1;
+  }
   auto probe = [&](const Item &it) {
     dep_ptr = nullptr;
     if (it.pos >= total) return;
