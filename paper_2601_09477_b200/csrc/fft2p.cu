@@ -23,6 +23,7 @@
 // self-paired slices (u2 = 0, N2/2) exchange partners through shared memory.
 // FA*FB is summed over the 32 lanes (k) in a fixed order and added to the
 // d x (b/2+1) accumulator in k-tile order (flags), so runs are bit-reproducible.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -597,10 +598,10 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
 static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
 static int init_w128(cudaStream_t s) {
-  static bool done[64] = {false};
+  static std::atomic<bool> done[64];  // idempotent: concurrent first calls copy the same table
   int dev = 0;
   SMM_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
-  if (dev < 64 && done[dev]) return SMM_OK;
+  if (dev < 64 && done[dev].load(std::memory_order_acquire)) return SMM_OK;
   double2 w[64];
   for (int j = 0; j < 64; ++j) {
     const double ang = M_PI * (double)j / 64.0;  // 2 pi j / 128
@@ -608,7 +609,7 @@ static int init_w128(cudaStream_t s) {
   }
   SMM_CUDA_TRY(cudaMemcpyToSymbolAsync(c_w128, w, sizeof(w), 0, cudaMemcpyHostToDevice, s), "w128 table");
   SMM_CUDA_TRY(cudaStreamSynchronize(s), "w128 table");
-  if (dev < 64) done[dev] = true;
+  if (dev < 64) done[dev].store(true, std::memory_order_release);
   return SMM_OK;
 }
 

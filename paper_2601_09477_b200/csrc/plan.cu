@@ -28,16 +28,18 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launches() { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
-  static int cached[64] = {0};
+  static std::atomic<int> cached[64];  // per-device attribute cache (idempotent fill)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (!cached[dev]) {
+  int c = cached[dev].load(std::memory_order_relaxed);
+  if (!c) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached[dev] = v > 0 ? v : 1;
+    c = v > 0 ? v : 1;
+    cached[dev].store(c, std::memory_order_relaxed);
   }
-  return cached[dev];
+  return c;
 }
 
 void load_hashes(SketchHashes &h, const uint64_t *words, int d, int log2b) {

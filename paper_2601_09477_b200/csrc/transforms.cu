@@ -4,6 +4,8 @@
 //
 // Reference: sketch.py:178-188 (FWHT inverse + 1/b), sketch.py:219-234 (FFT
 // Hermitian fill + inverse + Re/b), transforms.py:37-175, sketch.py:305-307.
+#include <atomic>
+
 #include "common.cuh"
 
 namespace smm {
@@ -117,15 +119,15 @@ __global__ void cscale_kernel(cplx *z, int64_t n, double scale) {
 // to the driver and the next cudaMallocAsync maps it again (milliseconds of host
 // time while the GPU idles).  Keep freed blocks in the pool.
 static void keep_pool_memory() {
-  static bool done[64] = {false};
+  static std::atomic<bool> done[64];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || done[dev]) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || done[dev].load(std::memory_order_relaxed)) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  done[dev] = true;
+  done[dev].store(true, std::memory_order_relaxed);
 }
 
 int fft_batched(cplx *z, int64_t batch, int log2n, int inverse, double scale, cudaStream_t s) {
