@@ -238,18 +238,26 @@ def run_ours(args) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    # warm-up holds the previous step's outputs while the next step runs, exactly as the timed
+    # loop does, so the caching allocator reaches its steady state (no cudaMalloc while timed)
+    sk = est = pairs = None
     for _ in range(args.warmup):
-        step()
+        sk, est, pairs = step()
     barrier()
     launches0 = lib.smm_kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record()
+        evs = []
         for _ in range(args.steps):
             sk, est, pairs = step()
+            evs.append(torch.cuda.Event(enable_timing=True))
+            evs[-1].record()
         ev1.record()
         barrier()
+    per_step = [ev0.elapsed_time(evs[0])] + [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]
+    print("per-step ms: " + " ".join(f"{x:.2f}" for x in per_step), file=sys.stderr, flush=True)
     launches = lib.smm_kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms], device=dev)

@@ -418,7 +418,8 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   const int hmask = (1 << hb) - 1;
   const int64_t lo0 = (int64_t)s << (P1_BITS - hb);
   // this lane's accumulator bucket after the lane reduction (fixed by the mapping)
-  const int sg_acc = hb > 5 ? ((lane & 3) | (warp << 2) | ((lane >> 2) << 5)) : (lane | (warp << 5));
+  const int rl = tp::lane_sum32_reg(lane);
+  const int sg_acc = hb > 5 ? ((rl & 3) | (warp << 2) | ((rl >> 2) << 5)) : (rl | (warp << 5));
   double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)(sg_acc & hmask) * 256 + lo0 + (sg_acc >> hb);
   // usually the previous k-tile's update of this slice finished long ago: fetch the old value early
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
@@ -494,7 +495,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
       double fa[8];
       tmem_ld8(tq + col_fa + 16 * c, fa);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[c + 4 * j] *= fa[j];
+      for (int j = 0; j < 8; ++j) v[c + 4 * j] = __dmul_rn(v[c + 4 * j], fa[j]);
     }
   } else {
 #pragma unroll 1
@@ -539,13 +540,245 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
     double fa[8];
     tmem_ld8(tq + col_fa + 16 * c, fa);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[8 * c + q] *= fa[q];
+    for (int q = 0; q < 8; ++q) v[8 * c + q] = __dmul_rn(v[8 * c + q], fa[q]);
   }
   }
   // sum over the 32 inner indices (lanes): lane l ends with register l summed over all lanes
   const double sum = tp::lane_sum32(v, lane);
   if (kappa == 0) {
     // accumulate mode continues a previous call's k order exactly (chunk boundaries are k-tiles)
+    __stcg(a, p.acc_add ? acc_old + sum : sum);
+  } else if (acc_ready) {
+    __stcg(a, acc_old + sum);
+  } else {
+    if (lane == 0)
+      while (flag < kappa) {
+        __nanosleep(32);
+        flag = ld_relaxed(acc_flag);
+      }
+    __syncwarp();
+    __stcg(a, __ldcg(a) + sum);
+  }
+}
+
+// ------------------------------------------------------------------ pair mapping
+// Used when both operands allow 16-byte accesses (even row stride, even k origin
+// and inner range, 16-byte aligned base) and the slice is 2^16 wide (hb = 8).
+// Lane = (lb, kp): kp = lane & 15 owns the inner-index pair (2 kp, 2 kp + 1) of
+// the k-tile as one double2, lb = lane >> 4 is one bucket bit; a thread holds
+// 16 buckets x 2 inner indices.  Against the one-k-per-lane mapping above this
+// halves the global and shared-memory instructions (every gather, Y store, Y
+// load and exchange access moves 16 bytes), and the sum over the 32 inner
+// indices starts with the in-thread pair, so the lane reduction has 4 halving
+// steps instead of 5.  Bucket bits of a 256-bucket block / slice:
+//   phase A: register j = bits 0-3, lb = bit 4, warp = bits 5-7
+//   phase B (after the one shared-memory exchange): warp = bits 0-2,
+//            lb = bit 3, register j = bits 4-7
+// Exchange cell of (beta, kp): S2[beta * 16 + kp] (64 KB, as before).
+__device__ __forceinline__ double2 ldg_pair(const char *p) { return __ldg((const double2 *)p); }
+
+__device__ __forceinline__ double2 d2_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 d2_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+__device__ __forceinline__ void reg_fwht16x2(double2 (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int h = 1 << q;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (!(j & h)) {
+        const double2 x = v[j], y = v[j + h];
+        v[j] = d2_add(x, y);
+        v[j + h] = d2_sub(x, y);
+      }
+  }
+}
+
+// CSR range of this lane's half-warp (16 buckets) and its first 16 entry words (one per kp)
+__device__ __forceinline__ PullHead pull_head2(const TwoPassArgs &p, int t, int op, int blk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blk * 256 + warp * 32 + (lane & 16);
+  const int64_t row = (int64_t)t * 2 + op;
+  const int32_t *off = p.off + row * (p.bsz + 1);
+  PullHead h;
+  h.e_lo = __ldg(off + base);
+  h.e_hi = __ldg(off + base + 16);
+  h.first = h.e_lo + (lane & 15) < h.e_hi ? __ldg(p.ent + row * p.nmax + h.e_lo + (lane & 15)) : 0u;
+  return h;
+}
+
+__device__ __forceinline__ const char *pair_row_base(const TwoPassArgs &p, int kappa, int op) {
+  const int64_t kk = (int64_t)kappa * KT + 2 * (threadIdx.x & 15);
+  return (const char *)(p.X[op] + p.k0 + (kk < p.K ? kk : p.K - 2));  // K even in pair mode
+}
+
+__device__ __forceinline__ void gather_first2(const TwoPassArgs &p, int kappa, int op, const PullHead &hd,
+                                              double2 (&x)[4]) {
+  const char *Xb = pair_row_base(p, kappa, op);
+  const uint32_t ldb = (uint32_t)(p.ld[op] * 8);
+  const int cnt = hd.e_hi - hd.e_lo;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const uint32_t e = __shfl_sync(0xffffffffu, hd.first, (lane & 16) | s);
+    x[s] = s < cnt ? ldg_pair(Xb + (uint64_t)(e & 0x03ffffffu) * ldb) : make_double2(0.0, 0.0);
+  }
+}
+
+__device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
+                                            double2 *S, const PullHead &hd, double2 (&xpre)[4], bool have_pre,
+                                            const PullHead *next) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kp = lane & 15, lb = lane >> 4;
+  const int64_t kk = (int64_t)kappa * KT + 2 * kp;
+  const bool full_tile = (int64_t)kappa * KT + KT <= p.K;  // warp-uniform
+  const char *Xb = pair_row_base(p, kappa, op);
+  const uint32_t ldb = (uint32_t)(p.ld[op] * 8);
+  const int64_t row = (int64_t)t * 2 + op;
+  const uint32_t *ent = p.ent + row * p.nmax + hd.e_lo;
+  const int cnt = hd.e_hi - hd.e_lo;
+  const int cnt_o = __shfl_xor_sync(0xffffffffu, cnt, 16);
+  const int cmax = cnt > cnt_o ? cnt : cnt_o;
+  // this lane's cells: beta = j | lb << 4 | warp << 5, j = 0..15 (lane-private: no barrier)
+  double2 *col = S + (warp * 32 + lb * 16) * 16 + kp;
+  uint32_t mask = 0;
+  int prevj = -1;
+  uint32_t win = hd.first;  // entry words [wbase, wbase + 16) of this half, one per kp
+  int wbase = 0;
+  for (int eb = 0; eb < cmax; eb += 4) {
+    if (eb - wbase == 16) {
+      wbase = eb;
+      win = eb + kp < cnt ? __ldg(ent + eb + kp) : 0u;
+    }
+    uint32_t es[4];
+    double2 x[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) es[s] = __shfl_sync(0xffffffffu, win, (lane & 16) | ((eb - wbase) + s));
+    if (have_pre && eb == 0) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) x[s] = xpre[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        x[s] = eb + s < cnt ? ldg_pair(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (eb + s < cnt) {
+        const int j = (int)((es[s] >> 26) & 15u);
+        uint32_t neg = es[s] >> 31;
+        if (p.F > 1)  // fold character of slice a: (-1)^popcount(a & (h(i) >> LB))
+          neg ^= __popc((eval_bucket(p.h.f[op][t], (uint64_t)(es[s] & 0x03ffffffu), p.B) >> p.LB) & (uint32_t)a) & 1u;
+        const double2 val = neg ? make_double2(-x[s].x, -x[s].y) : x[s];
+        const double2 old = j == prevj ? col[j * 16] : make_double2(0.0, 0.0);  // 0 + val == val
+        col[j * 16] = d2_add(old, val);
+        mask |= 1u << j;
+        prevj = j;
+      }
+    }
+  }
+  double2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? col[j * 16] : make_double2(0.0, 0.0);
+  if (!full_tile && kk >= p.K) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = make_double2(0.0, 0.0);
+  }
+  PROF_MARK(3);
+  reg_fwht16x2(v);  // bucket bits 0-3
+#pragma unroll
+  for (int j = 0; j < 16; ++j) col[j * 16] = v[j];
+  PROF_MARK(4);
+  __syncthreads();
+  PROF_MARK(5);
+  // phase B: beta = warp | lb << 3 | j << 4
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = S[((warp | (lb << 3) | (j << 4)) * 16) + kp];
+  reg_fwht16x2(v);  // bucket bits 4-7
+  PROF_MARK(6);
+  if (next) gather_first2(p, kappa, 1, *next, xpre);
+  double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 256) * KT + 2 * kp;
+  const uint64_t pol = policy_evict_last();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int beta = warp | (lb << 3) | (j << 4);
+    tp::st2_hint(Yd + (int64_t)beta * KT, v[j].x, v[j].y, pol);
+  }
+  PROF_MARK(7);
+}
+
+__device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double2 *S,
+                                         const PullHead &hd1, const PullHead &hd0) {
+  double2 xpre[4];
+  p1_operand2(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
+  __syncthreads();  // every warp has read operand 0's exchange data from S
+  p1_operand2(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
+}
+
+// Pass 2 of slice s (hb = 8: the 256 buckets eta * 256 + s), pair mapping.
+__device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s,
+                                         uint32_t tmem, const int *acc_flag, double2 *S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kp = lane & 15, lb = lane >> 4;
+  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
+  // after the lane reduction lane (lb, kp) of warp w holds eta = w | lb << 3 | kp << 4
+  const int eta_acc = warp | (lb << 3) | (kp << 4);
+  double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)eta_acc * 256 + s;
+  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
+  const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
+  const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+  const uint32_t col_fa = (uint32_t)((warp >> 2) * 64);
+  const uint64_t pol = policy_evict_first();
+  double2 *cell = S + (warp * 32 + lb * 16) * 16 + kp;  // phase-A cells of this lane (j * 16 apart)
+  double2 v[16];
+#pragma unroll 1
+  for (int op = 0; op < 2; ++op) {
+    const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + 2 * kp;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int eta = j | (lb << 4) | (warp << 5);
+      tp::ld2_hint(Ys + ((int64_t)eta * 256 + s) * KT, v[j].x, v[j].y, pol);
+    }
+    PROF_MARK(8);
+    reg_fwht16x2(v);  // eta bits 0-3
+    // last use of these Y rows (all read by this warp): drop the L2 lines without write-back
+    __syncwarp();
+    {
+      const double *rowp = Ys - 2 * kp + ((int64_t)(lane | (warp << 5)) * 256 + s) * KT;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cell[j * 16] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = S[((warp | (lb << 3) | (j << 4)) * 16) + kp];
+    reg_fwht16x2(v);  // eta bits 4-7
+    if (op == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st8(tq + col_fa + 16 * c, (const double *)(v + 4 * c));
+      tmem_wait_st();
+      __syncthreads();  // S is reused by operand 1's exchange (the next item's waits for [B])
+    }
+  }
+  PROF_MARK(9);
+  // product FA * FB, summed over the thread's inner-index pair
+  double pr[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double fa[8];
+    tmem_ld8(tq + col_fa + 16 * c, fa);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // products rounded, then the pair sum: the first node of lane_sum32's tree
+      pr[4 * c + q] = __dadd_rn(__dmul_rn(v[4 * c + q].x, fa[2 * q]), __dmul_rn(v[4 * c + q].y, fa[2 * q + 1]));
+  }
+  // sum over the 16 pairs (lane bits 3..0 = inner-index bits 4..1): lane kp ends with register kp
+  tp::halve_step<8, 8>(pr, lane);
+  tp::halve_step<4, 4>(pr, lane);
+  tp::halve_step<2, 2>(pr, lane);
+  tp::halve_step<1, 1>(pr, lane);
+  const double sum = pr[0];
+  if (kappa == 0) {
     __stcg(a, p.acc_add ? acc_old + sum : sum);
   } else if (acc_ready) {
     __stcg(a, acc_old + sum);
@@ -595,7 +828,7 @@ __device__ __forceinline__ void red_add(int *ptr, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
 }
 
-template <int HB>
+template <int HB, bool PAIR>
 __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   extern __shared__ __align__(16) double S[];  // 8 warps x 32 x 32 doubles = 64 KB
   __shared__ uint32_t s_tmem;
@@ -709,17 +942,24 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     }
     if (!go) break;
     PullHead hd_cur, hd_cur1;
+    auto head = [&](int tt, int op, int blk) { return PAIR ? pull_head2(p, tt, op, blk) : pull_head(p, tt, op, blk); };
     if (is_p1) {
-      hd_cur = hd_valid ? hd_next : pull_head(p, t, 0, idx);
-      hd_cur1 = hd_valid ? hd_next1 : pull_head(p, t, 1, idx);
+      hd_cur = hd_valid ? hd_next : head(t, 0, idx);
+      hd_cur1 = hd_valid ? hd_next1 : head(t, 1, idx);
     }
     hd_valid = next_p1 != 0;
     if (hd_valid) {  // land while this item computes
-      hd_next = pull_head(p, next_t, 0, next_idx);
-      hd_next1 = pull_head(p, next_t, 1, next_idx);
+      hd_next = head(next_t, 0, next_idx);
+      hd_next1 = head(next_t, 1, next_idx);
     }
-    if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
-    else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_cnt + (t * p.F + asl) * p.nblk + idx, S);
+    const int *acc_flag = acc_cnt + (t * p.F + asl) * p.nblk + idx;
+    if constexpr (PAIR) {
+      if (is_p1) p1_item2(p, kappa, t, asl, slot, idx, (double2 *)S, hd_cur1, hd_cur);
+      else p2_item2(p, kappa, t, asl, slot, idx, tmem, acc_flag, (double2 *)S);
+    } else {
+      if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
+      else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, S);
+    }
     tc_fence_before();
     PROF_MARK(2);
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
@@ -906,12 +1146,20 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   // two persistent CTAs per SM (256 threads, 128 registers, 64 KB smem, 128 TMEM columns each):
   // one CTA's barriers and memory latency overlap the other's FP64 work
   const int G = 2 * num_sms();
-  switch (p.hb) {
+  // pair mapping: 16-byte operand rows need an even k origin, stride and range and an aligned base
+  static const bool pair_off = getenv("SMM_NO_PAIR") != nullptr;
+  const bool pair = !pair_off && p.hb == 8 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
+                    ((uintptr_t)xa % 16) == 0 && ((uintptr_t)xb % 16) == 0;
+  if (pair) {
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                 "fwht2p smem");
+    fwht2p_kernel<8, true><<<G, P_THREADS, smem, s>>>(p);
+  } else switch (p.hb) {
 #define SMM_LAUNCH_HB(H)                                                                                 \
   case H:                                                                                                \
-    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
                  "fwht2p smem");                                                                         \
-    fwht2p_kernel<H><<<G, P_THREADS, smem, s>>>(p);                                                      \
+    fwht2p_kernel<H, false><<<G, P_THREADS, smem, s>>>(p);                                               \
     break;
     SMM_LAUNCH_HB(0) SMM_LAUNCH_HB(1) SMM_LAUNCH_HB(2) SMM_LAUNCH_HB(3)
     SMM_LAUNCH_HB(4) SMM_LAUNCH_HB(5) SMM_LAUNCH_HB(6) SMM_LAUNCH_HB(7) SMM_LAUNCH_HB(8)

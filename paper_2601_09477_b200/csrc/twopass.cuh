@@ -94,25 +94,33 @@ static __device__ __forceinline__ void ld2_hint(const double *p, double &a, doub
 }
 
 // Sum over the 32 lanes of a warp, for each of 32 registers: recursive halving
-// through shuffles (31 double shuffles per lane, no shared memory).  Lane l ends
-// with register l summed over all lanes.
-template <int H>
-static __device__ __forceinline__ void halve_step(double (&v)[32], int lane) {
-  const bool hi = (lane & H) != 0;
+// through shuffles (31 double shuffles per lane, no shared memory).  Step
+// (L, R): lanes differing in lane bit L exchange register halves [0, R) / [R, 2R).
+// The lane bits are combined in the order 1, 16, 8, 4, 2 — the same summation
+// tree as the pair mapping of fwht2p (in-thread pair (2kp, 2kp+1) first, then
+// kp bits 3..0), so both mappings give bit-identical accumulators.  Lane l ends
+// with register lane_sum32_reg(l) summed over all lanes.
+template <int L, int R, int N>
+static __device__ __forceinline__ void halve_step(double (&v)[N], int lane) {
+  const bool hi = (lane & L) != 0;
 #pragma unroll
-  for (int r = 0; r < H; ++r) {
-    const double send = hi ? v[r] : v[r + H];
-    const double keep = hi ? v[r + H] : v[r];
-    v[r] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+  for (int r = 0; r < R; ++r) {
+    const double send = hi ? v[r] : v[r + R];
+    const double keep = hi ? v[r + R] : v[r];
+    v[r] = keep + __shfl_xor_sync(0xffffffffu, send, L);
   }
 }
 
+static __device__ __forceinline__ int lane_sum32_reg(int l) {
+  return ((l & 1) << 4) | (((l >> 4) & 1) << 3) | (((l >> 3) & 1) << 2) | (((l >> 2) & 1) << 1) | ((l >> 1) & 1);
+}
+
 static __device__ __forceinline__ double lane_sum32(double (&v)[32], int lane) {
-  halve_step<16>(v, lane);
-  halve_step<8>(v, lane);
-  halve_step<4>(v, lane);
-  halve_step<2>(v, lane);
-  halve_step<1>(v, lane);
+  halve_step<1, 16>(v, lane);
+  halve_step<16, 8>(v, lane);
+  halve_step<8, 4>(v, lane);
+  halve_step<4, 2>(v, lane);
+  halve_step<2, 1>(v, lane);
   return v[0];
 }
 
