@@ -575,6 +575,10 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
 //   phase B (after the one shared-memory exchange): warp = bits 0-2,
 //            lb = bit 3, register j = bits 4-7
 // Exchange cell of (beta, kp): S2[beta * 16 + kp] (64 KB, as before).
+#ifndef SMM_PGB
+#define SMM_PGB 6
+#endif
+constexpr int PGB = SMM_PGB;  // gather batch (entries per half-warp in flight)
 __device__ __forceinline__ double2 ldg_pair(const char *p) { return __ldg((const double2 *)p); }
 
 __device__ __forceinline__ double2 d2_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -613,20 +617,20 @@ __device__ __forceinline__ const char *pair_row_base(const TwoPassArgs &p, int k
 }
 
 __device__ __forceinline__ void gather_first2(const TwoPassArgs &p, int kappa, int op, const PullHead &hd,
-                                              double2 (&x)[4]) {
+                                              double2 (&x)[PGB]) {
   const char *Xb = pair_row_base(p, kappa, op);
   const uint32_t ldb = (uint32_t)(p.ld[op] * 8);
   const int cnt = hd.e_hi - hd.e_lo;
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < PGB; ++s) {
     const uint32_t e = __shfl_sync(0xffffffffu, hd.first, (lane & 16) | s);
     x[s] = s < cnt ? ldg_pair(Xb + (uint64_t)(e & 0x03ffffffu) * ldb) : make_double2(0.0, 0.0);
   }
 }
 
 __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
-                                            double2 *S, const PullHead &hd, double2 (&xpre)[4], bool have_pre,
+                                            double2 *S, const PullHead &hd, double2 (&xpre)[PGB], bool have_pre,
                                             const PullHead *next) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kp = lane & 15, lb = lane >> 4;
@@ -645,25 +649,25 @@ __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int
   int prevj = -1;
   uint32_t win = hd.first;  // entry words [wbase, wbase + 16) of this half, one per kp
   int wbase = 0;
-  for (int eb = 0; eb < cmax; eb += 4) {
-    if (eb - wbase == 16) {
+  for (int eb = 0; eb < cmax; eb += PGB) {
+    if (eb - wbase + PGB > 16) {  // window exhausted (16 % PGB == 0, or refetch early)
       wbase = eb;
       win = eb + kp < cnt ? __ldg(ent + eb + kp) : 0u;
     }
-    uint32_t es[4];
-    double2 x[4];
+    uint32_t es[PGB];
+    double2 x[PGB];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) es[s] = __shfl_sync(0xffffffffu, win, (lane & 16) | ((eb - wbase) + s));
+    for (int s = 0; s < PGB; ++s) es[s] = __shfl_sync(0xffffffffu, win, (lane & 16) | ((eb - wbase) + s));
     if (have_pre && eb == 0) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) x[s] = xpre[s];
+      for (int s = 0; s < PGB; ++s) x[s] = xpre[s];
     } else {
 #pragma unroll
-      for (int s = 0; s < 4; ++s)
+      for (int s = 0; s < PGB; ++s)
         x[s] = eb + s < cnt ? ldg_pair(Xb + (uint64_t)(es[s] & 0x03ffffffu) * ldb) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < PGB; ++s) {
       if (eb + s < cnt) {
         const int j = (int)((es[s] >> 26) & 15u);
         uint32_t neg = es[s] >> 31;
@@ -709,7 +713,7 @@ __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int
 
 __device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double2 *S,
                                          const PullHead &hd1, const PullHead &hd0) {
-  double2 xpre[4];
+  double2 xpre[PGB];
   p1_operand2(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
   __syncthreads();  // every warp has read operand 0's exchange data from S
   p1_operand2(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
