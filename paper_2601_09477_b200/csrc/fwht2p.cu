@@ -584,9 +584,10 @@ __device__ __forceinline__ double2 ldg_pair(const char *p) { return __ldg((const
 __device__ __forceinline__ double2 d2_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 d2_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
-__device__ __forceinline__ void reg_fwht16x2(double2 (&v)[16]) {
+__device__ __forceinline__ void reg_fwht16x2(double2 (&v)[16], int nq = 4) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    if (q >= nq) break;
     const int h = 1 << q;
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -719,15 +720,20 @@ __device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t,
   p1_operand2(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
 }
 
-// Pass 2 of slice s (hb = 8: the 256 buckets eta * 256 + s), pair mapping.
+// Pass 2 of slice s, pair mapping: slice position pi (8 bits) is bucket
+// (pi & hmask) * 256 + lo0 + (pi >> hb); the hb low bits of pi are transformed
+// (5 <= hb <= 8: phase A bits 0-3, phase B bits 4..hb-1).
+template <int HB>
 __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s,
                                          uint32_t tmem, const int *acc_flag, double2 *S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kp = lane & 15, lb = lane >> 4;
   int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
   // after the lane reduction lane (lb, kp) of warp w holds eta = w | lb << 3 | kp << 4
-  const int eta_acc = warp | (lb << 3) | (kp << 4);
-  double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)eta_acc * 256 + s;
+  constexpr int hmask = (1 << HB) - 1;
+  const int64_t lo0 = (int64_t)s << (P1_BITS - HB);
+  auto row_of = [&](int pi) { return (int64_t)(pi & hmask) * 256 + lo0 + (pi >> HB); };
+  double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + row_of(warp | (lb << 3) | (kp << 4));
   const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
@@ -740,15 +746,14 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + 2 * kp;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int eta = j | (lb << 4) | (warp << 5);
-      tp::ld2_hint(Ys + ((int64_t)eta * 256 + s) * KT, v[j].x, v[j].y, pol);
+      tp::ld2_hint(Ys + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
     }
     PROF_MARK(8);
     reg_fwht16x2(v);  // eta bits 0-3
     // last use of these Y rows (all read by this warp): drop the L2 lines without write-back
     __syncwarp();
     {
-      const double *rowp = Ys - 2 * kp + ((int64_t)(lane | (warp << 5)) * 256 + s) * KT;
+      const double *rowp = Ys - 2 * kp + row_of(lane | (warp << 5)) * KT;
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
     }
@@ -757,7 +762,7 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = S[((warp | (lb << 3) | (j << 4)) * 16) + kp];
-    reg_fwht16x2(v);  // eta bits 4-7
+    reg_fwht16x2(v, HB - 4);  // pi bits 4..hb-1
     if (op == 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_st8(tq + col_fa + 16 * c, (const double *)(v + 4 * c));
@@ -959,7 +964,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     const int *acc_flag = acc_cnt + (t * p.F + asl) * p.nblk + idx;
     if constexpr (PAIR) {
       if (is_p1) p1_item2(p, kappa, t, asl, slot, idx, (double2 *)S, hd_cur1, hd_cur);
-      else p2_item2(p, kappa, t, asl, slot, idx, tmem, acc_flag, (double2 *)S);
+      else p2_item2<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, (double2 *)S);
     } else {
       if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
       else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, S);
@@ -1152,12 +1157,18 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   const int G = 2 * num_sms();
   // pair mapping: 16-byte operand rows need an even k origin, stride and range and an aligned base
   static const bool pair_off = getenv("SMM_NO_PAIR") != nullptr;
-  const bool pair = !pair_off && p.hb == 8 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
+  const bool pair = !pair_off && p.hb >= 5 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
                     ((uintptr_t)xa % 16) == 0 && ((uintptr_t)xb % 16) == 0;
-  if (pair) {
-    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                 "fwht2p smem");
-    fwht2p_kernel<8, true><<<G, P_THREADS, smem, s>>>(p);
+  if (pair) switch (p.hb) {
+#define SMM_LAUNCH_PAIR(H)                                                                                      \
+  case H:                                                                                                       \
+    SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+                 "fwht2p smem");                                                                                \
+    fwht2p_kernel<H, true><<<G, P_THREADS, smem, s>>>(p);                                                       \
+    break;
+    SMM_LAUNCH_PAIR(5) SMM_LAUNCH_PAIR(6) SMM_LAUNCH_PAIR(7) SMM_LAUNCH_PAIR(8)
+#undef SMM_LAUNCH_PAIR
+    default: break;
   } else switch (p.hb) {
 #define SMM_LAUNCH_HB(H)                                                                                 \
   case H:                                                                                                \

@@ -415,3 +415,43 @@ def test_degenerate_hashes_everything_in_one_bucket(transform, log2b):
     polys = _device.finalize(acc, d, log2b, transform).cpu().numpy()
     ref = O.compress(a, bm, b=1 << log2b, d=d, words=words, transform=transform, seed=0, threads=8)
     assert np.abs(polys - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+_PAIR_CASE = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2601_09477_b200 import _device
+from oracle import sketch_oracle as O
+rng = np.random.default_rng(5)
+out = []
+for log2b, n in ((13, 700), (14, 1024), (15, 600), (16, 1500), (17, 900)):
+    a = torch.as_tensor(rng.standard_normal((n, 256)), device="cuda")
+    bt = torch.as_tensor(rng.standard_normal((n + 8, 256)), device="cuda")
+    words = O.draw_words(31 + log2b, 3, 1 << log2b)
+    acc = _device.compress_accumulate(a, bt, words, 3, log2b, "fwht", 0, 256,
+                                      a_layout=_device.KMINOR, b_layout=_device.KMINOR)
+    out.append(acc.cpu().numpy())
+np.savez({path!r}, *out)
+"""
+
+
+@pytest.mark.parametrize("_", [0])
+def test_pair_mapping_bit_identical_to_one_k_per_lane(tmp_path, _):
+    """The pair mapping of fwht2p (16-byte accesses, chosen automatically) and the
+    one-k-per-lane mapping (SMM_NO_PAIR=1) compute the same sums in the same
+    order: bit-identical accumulators on non-integer data."""
+    import os
+    import subprocess
+    import sys
+
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for tag, env in (("pair", {}), ("lane", {"SMM_NO_PAIR": "1"})):
+        path = str(tmp_path / f"{tag}.npz")
+        subprocess.run([sys.executable, "-c", _PAIR_CASE.format(root=root, path=path)], check=True,
+                       env={**os.environ, **env}, timeout=300)
+        g = np.load(path)
+        res[tag] = [g[f"arr_{i}"] for i in range(len(g.files))]
+    for x, y in zip(res["pair"], res["lane"]):
+        assert np.array_equal(x, y)
+        assert np.abs(x).max() > 0
