@@ -363,11 +363,14 @@ def test_two_pass_fft_against_oracle(log2b, n1, m, n2, d):
 
 @pytest.mark.parametrize("log2b,n1,m,n2,d", [(8, 3000, 70, 2000, 3), (10, 5000, 96, 4000, 5), (12, 9000, 45, 8000, 3),
                                              (14, 1000, 1, 900, 9), (16, 700, 33, 650, 3), (17, 400, 31, 350, 3),
-                                             (20, 300, 37, 280, 3)])
+                                             (20, 300, 37, 280, 3),
+                                             # even inner ranges: the pair mapping (b >= 2^13)
+                                             (13, 20000, 30, 300, 3), (13, 700, 34, 650, 3), (14, 3000, 62, 2000, 5),
+                                             (15, 500, 2, 450, 3), (16, 900, 46, 700, 3), (18, 400, 34, 350, 3)])
 def test_two_pass_fwht_against_oracle(log2b, n1, m, n2, d):
     # fwht2p across its whole range: dense pulls (n >> b: hundreds of CSR entries per warp,
-    # several 32-entry windows), a single inner index, partial k-tiles, the fold (b > 2^16),
-    # rectangular operands; against the oracle (reference algorithm) at 1e-12 relative
+    # several entry windows), a single inner index / pair, partial k-tiles, the fold (b > 2^16),
+    # rectangular operands, both lane mappings; against the oracle (reference algorithm) at 1e-12 relative
     rng = np.random.default_rng(log2b + 7)
     a = rng.standard_normal((n1, m))
     bm = rng.standard_normal((m, n2))
