@@ -16,6 +16,9 @@
 // operand's pass-2 result in TMEM until the product, sums FA*FB over the 32
 // lanes and adds it to the d x b accumulator once per k-tile.  b > 2^16 is
 // folded into F = b / 2^16 slices (one sign per entry).
+// Slices of 2^13..2^16 buckets use the *pair mapping* when the operands allow
+// 16-byte rows (see "pair mapping" below): lanes own inner-index pairs, 4 + 4
+// bucket bits per pass, bit-identical results with half the memory instructions.
 //
 // Scheduling: two persistent CTAs per SM pull tickets from a global counter in
 // a fixed order [P1(0..lag-1)] [P1(lag) P2(0)] [P1(lag+1) P2(1)] ... where a
