@@ -141,6 +141,14 @@ int smm_query(int variant, const double *polys, const uint64_t *words_host, int 
  * bench/evidence only). */
 int64_t smm_kernel_launches(void);
 
+/* Live per-launch kernel timing (bench evidence): while enabled, every launch of the
+ * compress kernel (channel 0: fwht2p / fft2p) and of the extraction kernel
+ * (channel 1) is bracketed by CUDA events on its stream.  _read waits for the
+ * recorded launches of a channel, returns their summed device time and count, and
+ * clears them.  Not a reference interface (the reference has no GPU). */
+int smm_kernel_timing(int enable);
+int smm_kernel_timing_read(int channel, double *total_ms, int64_t *launches);
+
 /* out[c, r] = in[r, c] for a rows x cols float64 matrix [dev]. */
 int smm_transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out,
                   int64_t ld_out, void *stream);

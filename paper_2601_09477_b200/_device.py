@@ -233,6 +233,19 @@ def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, l
     return acc
 
 
+def kernel_timing(enable: bool) -> None:
+    """Bracket every compress / extraction kernel launch with CUDA events (bench evidence)."""
+    _lib.check(_lib.load().smm_kernel_timing(1 if enable else 0))
+
+
+def kernel_timing_read(channel: int) -> tuple[float, int]:
+    """(summed device ms, launches) recorded on channel 0 (compress) or 1 (extraction); clears them."""
+    tot = ctypes.c_double(0.0)
+    cnt = ctypes.c_int64(0)
+    _lib.check(_lib.load().smm_kernel_timing_read(channel, ctypes.byref(tot), ctypes.byref(cnt)))
+    return float(tot.value), int(cnt.value)
+
+
 def finalize(acc: torch.Tensor, d: int, log2b: int, variant: str) -> torch.Tensor:
     lib = _lib.load()
     polys = torch.empty((d, 1 << log2b), dtype=torch.float64, device=acc.device)

@@ -39,6 +39,8 @@ EXPORTS = (
     "smm_hh_pairs",
     "smm_query",
     "smm_kernel_launches",
+    "smm_kernel_timing",
+    "smm_kernel_timing_read",
     "smm_transpose",
     "smm_copy2d",
     "smm_fwht_batched",
@@ -84,6 +86,8 @@ def load():
             "smm_extract": ([I, P, P, I, I, I64, I64, I64, I64, P, I64, D, I, P, I64, P, P, I64, P], I),
             "smm_hh_pairs": ([P, I64, I64, I64, P, I64, P], I),
             "smm_kernel_launches": ([], I64),
+            "smm_kernel_timing": ([I], I),
+            "smm_kernel_timing_read": ([I, P, P], I),
             "smm_transpose": ([P, I64, I64, I64, P, I64, P], I),
             "smm_copy2d": ([P, I64, P, I64, I64, I64, P], I),
             "smm_query": ([I, P, P, I, I, I64, I64, P, I64, P, P, P], I),

@@ -281,6 +281,17 @@ int smm_query(int variant, const double *polys, const uint64_t *words_host, int 
 
 int64_t smm_kernel_launches(void) { return launches(); }
 
+int smm_kernel_timing(int enable) {
+  kernel_timing(enable);
+  return SMM_OK;
+}
+
+int smm_kernel_timing_read(int channel, double *total_ms, int64_t *launches_out) {
+  SMM_REQUIRE(total_ms != nullptr && launches_out != nullptr, "NULL argument");
+  SMM_REQUIRE(channel == 0 || channel == 1, "channel must be 0 (compress) or 1 (extraction)");
+  return kernel_timing_read(channel, total_ms, launches_out);
+}
+
 int smm_transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out, int64_t ld_out,
                   void *stream) {
   SMM_REQUIRE(rows >= 0 && cols >= 0 && ld_in >= cols && ld_out >= rows, "bad transpose shape");

@@ -25,6 +25,20 @@ void count_launch();
 
 int num_sms();
 
+// Per-launch CUDA-event timing of the dominant kernels, for the bench's roofline
+// (smm_kernel_timing): when enabled, a KernelTimer records an event pair on the
+// launching stream around one launch of channel 0 (compress kernels) or 1 (extraction).
+struct KernelTimer {
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t s = nullptr;
+  int channel = 0;
+  KernelTimer(int channel, cudaStream_t s);
+  ~KernelTimer();  // an unstopped timer (error path) returns its events unrecorded
+  void stop();
+};
+void kernel_timing(int on);
+int kernel_timing_read(int channel, double *total_ms, int64_t *count);
+
 // ---------------------------------------------------------------- hashing
 // One drawn hash function (hashing.py:35-51): bucket = ((a*x + c) mod 2^64) >> shift.
 struct HashFn {

@@ -270,6 +270,7 @@ int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1,
   }
   SMM_CUDA_TRY(cudaMemsetAsync(p.rowcnt, 0, rows * 8, s), "extract memset");
   dim3 grid((unsigned)ceil_div(n2, XT), (unsigned)ceil_div(rows, XROWS));
+  KernelTimer timer(1, s);
   switch (h.d) {
     case 1: extract_kernel<1><<<grid, XT, 0, s>>>(p); break;
     case 3: extract_kernel<3><<<grid, XT, 0, s>>>(p); break;
@@ -278,6 +279,7 @@ int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1,
     case 9: extract_kernel<9><<<grid, XT, 0, s>>>(p); break;
     default: extract_kernel<0><<<grid, XT, 0, s>>>(p); break;
   }
+  timer.stop();
   SMM_LAUNCH_CHECK("extract_kernel");
   row_scan_kernel<<<1, 1024, 0, s>>>(p.rowcnt, rows, offs, hh_count);
   SMM_LAUNCH_CHECK("row_scan_kernel");

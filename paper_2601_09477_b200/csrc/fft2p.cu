@@ -792,6 +792,7 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
                  "fft2p smem");                                                                       \
     fft2p_kernel<SS, FD><<<G, THREADS, smem, s>>>(p);                                                 \
     break;
+  KernelTimer timer(0, s);
   switch (S1 + 8 * (g.F > 1 ? 1 : 0)) {
     F2P_LAUNCH(1, 0) F2P_LAUNCH(2, 0) F2P_LAUNCH(3, 0) F2P_LAUNCH(4, 0) F2P_LAUNCH(5, 0) F2P_LAUNCH(6, 0)
     F2P_LAUNCH(7, 0) F2P_LAUNCH(7, 1)
@@ -800,6 +801,7 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
       set_error("two-pass fft kernel: unsupported width");
       return SMM_ERR_INVALID;
   }
+  timer.stop();
   SMM_LAUNCH_CHECK("fft2p_kernel");
   return SMM_OK;
 }

@@ -1162,6 +1162,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   static const bool pair_off = getenv("SMM_NO_PAIR") != nullptr;
   const bool pair = !pair_off && p.hb >= 5 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
                     ((uintptr_t)xa % 16) == 0 && ((uintptr_t)xb % 16) == 0;
+  KernelTimer timer(0, s);
   if (pair) switch (p.hb) {
 #define SMM_LAUNCH_PAIR(H)                                                                                      \
   case H:                                                                                                       \
@@ -1186,6 +1187,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
       set_error("two-pass kernel: unsupported width");
       return SMM_ERR_INVALID;
   }
+  timer.stop();
   SMM_LAUNCH_CHECK("fwht2p_kernel");
   if (p.prof) {
     long long h[16];

@@ -1,7 +1,10 @@
 // Hash tables and scatter plans (see plan.cuh).
 #include <cstdarg>
 #include <atomic>
+#include <array>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "plan.cuh"
 
@@ -26,6 +29,67 @@ int cuda_status(cudaError_t e, const char *what) {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launches() { return (int64_t)g_launches.load(std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ kernel timing (evidence)
+static std::atomic<int> g_timing{0};
+static std::mutex g_tmx;
+static std::vector<std::array<cudaEvent_t, 2>> g_tpool;                 // idle event pairs
+static std::vector<std::pair<int, std::array<cudaEvent_t, 2>>> g_tdone;  // (channel, recorded pair)
+
+KernelTimer::KernelTimer(int ch, cudaStream_t st) : s(st), channel(ch) {
+  if (!g_timing.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> g(g_tmx);
+  if (g_tpool.empty()) {
+    std::array<cudaEvent_t, 2> e{};
+    if (cudaEventCreate(&e[0]) != cudaSuccess || cudaEventCreate(&e[1]) != cudaSuccess) return;
+    g_tpool.push_back(e);
+  }
+  ev[0] = g_tpool.back()[0];
+  ev[1] = g_tpool.back()[1];
+  g_tpool.pop_back();
+  cudaEventRecord(ev[0], s);
+}
+
+KernelTimer::~KernelTimer() {
+  if (!ev[0]) return;
+  std::lock_guard<std::mutex> g(g_tmx);
+  g_tpool.push_back({ev[0], ev[1]});
+}
+
+void KernelTimer::stop() {
+  if (!ev[0]) return;
+  cudaEventRecord(ev[1], s);
+  std::lock_guard<std::mutex> g(g_tmx);
+  g_tdone.push_back({channel, {ev[0], ev[1]}});
+  ev[0] = ev[1] = nullptr;
+}
+
+void kernel_timing(int on) { g_timing.store(on ? 1 : 0, std::memory_order_relaxed); }
+
+// sums and clears the recorded launches of `channel` (waits for their end events)
+int kernel_timing_read(int channel, double *total_ms, int64_t *count) {
+  std::lock_guard<std::mutex> g(g_tmx);
+  double tot = 0.0;
+  int64_t n = 0;
+  std::vector<std::pair<int, std::array<cudaEvent_t, 2>>> keep;
+  for (auto &r : g_tdone) {
+    if (r.first != channel) {
+      keep.push_back(r);
+      continue;
+    }
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.second[1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.second[0], r.second[1]);
+    if (e != cudaSuccess) return cuda_status(e, "kernel timing");
+    tot += ms;
+    ++n;
+    g_tpool.push_back(r.second);
+  }
+  g_tdone.swap(keep);
+  *total_ms = tot;
+  *count = n;
+  return SMM_OK;
+}
 
 int num_sms() {
   static std::atomic<int> cached[64];  // per-device attribute cache (idempotent fill)

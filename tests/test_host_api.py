@@ -153,6 +153,12 @@ def test_abi_rejects_bad_parameters_before_any_kernel():
     assert b"NULL" in lib.smm_last_error() or b"range" in lib.smm_last_error()
     assert lib.smm_extract_workspace(3, 8, 8, 4, 9, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
     assert lib.smm_compress_workspace(1, 3, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_OK and out.value > 0
+    # live kernel timing: nothing recorded yet, bad channel rejected
+    tot, cnt = ctypes.c_double(-1.0), ctypes.c_int64(-1)
+    assert lib.smm_kernel_timing(0) == _lib.SMM_OK
+    assert lib.smm_kernel_timing_read(0, ctypes.byref(tot), ctypes.byref(cnt)) == _lib.SMM_OK
+    assert tot.value == 0.0 and cnt.value == 0
+    assert lib.smm_kernel_timing_read(2, ctypes.byref(tot), ctypes.byref(cnt)) == _lib.SMM_ERR_INVALID
 
 
 def test_api_validates_before_device_work():
