@@ -1,0 +1,155 @@
+"""Property tests of the sketch, on the CUDA path — the reference's own test
+classes (pkg/tests/test_sketch.py) restated against this implementation:
+
+* zero operands give a zero sketch and zero estimates (test_sketch.py:93-98);
+* mass preservation: each repetition's coefficients sum to the signed grand
+  total of C (test_sketch.py:111-131);
+* exact recovery with an injective index map (the pinned seeds of
+  test_sketch.py:30, 141-159);
+* noise decomposition: an estimate is the truth plus the signed sum of the
+  entries sharing its bucket (test_sketch.py:230-254);
+* unbiasedness over 4000 hash seeds and the variance bound 1.3 ||C||_F^2 / b
+  over 3000 seeds (test_sketch.py:193-226) — here through compress_seeds, the
+  batched Monte-Carlo mode;
+* the one-shot transforms (pkg/tests/test_transforms.py): dense-Hadamard closed
+  form, involution, Parseval, XOR / cyclic convolution against brute force, the
+  half-spectrum FFT against numpy.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2601_09477_b200 as P
+from paper_2601_09477_b200.hashing import SketchHashes, eval_bucket, eval_sign
+
+pytestmark = pytest.mark.gpu
+
+INJECTIVE_SEED = {"fwht": 5, "fft": 12}  # reference test_sketch.py:30
+
+
+def _pair(rng, n):
+    return rng.normal(size=(n, n)), rng.normal(size=(n, n))
+
+
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+def test_zero_operands(transform):
+    p = P.SketchParams(n=8, b=16, d=3, transform=transform, seed=1)
+    sk = P.compress(np.zeros((8, 8)), np.zeros((8, 8)), p)
+    assert np.array_equal(sk.polys, np.zeros((3, 16)))
+    assert np.array_equal(P.decompress_all(sk), np.zeros((8, 8)))
+
+
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+@pytest.mark.parametrize("n,b", [(8, 32), (300, 1 << 13), (256, 1 << 16)])
+def test_polynomial_mass_preserved(transform, n, b):
+    rng = np.random.default_rng(4)
+    a, m = _pair(rng, n)
+    c = a @ m
+    d = 5
+    p = P.SketchParams(n=n, b=b, d=d, transform=transform, seed=3)
+    sk = P.compress(a, m, p)
+    s1 = sk.hashes.sign_table("s1", n)
+    s2 = sk.hashes.sign_table("s2", n)
+    want = np.array([np.sum(s1[t][:, None] * s2[t][None, :] * c) for t in range(d)])
+    scale = max(1.0, float(np.linalg.norm(c)))
+    assert np.max(np.abs(sk.polys.sum(axis=1) - want)) <= 1e-9 * scale
+
+
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+def test_injective_hash_recovers_exactly(transform):
+    seed = INJECTIVE_SEED[transform]
+    hashes = SketchHashes.draw(np.random.default_rng(seed), 1, 16)
+    u = np.array([eval_bucket(hashes.h1[0], x) for x in range(4)])
+    v = np.array([eval_bucket(hashes.h2[0], x) for x in range(4)])
+    combined = (u[:, None] ^ v[None, :]) if transform == "fwht" else (u[:, None] + v[None, :]) % 16
+    assert len(np.unique(combined)) == 16, "pinned seed no longer injective"
+    a, m = _pair(np.random.default_rng(0), 4)
+    p = P.SketchParams(n=4, b=16, d=1, transform=transform, seed=seed)
+    est = P.decompress_all(P.compress(a, m, p))
+    assert np.max(np.abs(est - a @ m)) < 1e-9
+
+
+def test_noise_decomposition():
+    n, b = 8, 16
+    a, m = _pair(np.random.default_rng(9), n)
+    truth = a @ m
+    p = P.SketchParams(n=n, b=b, d=1, transform="fwht", seed=4)
+    sk = P.compress(a, m, p)
+    h = sk.hashes
+    est = P.decompress_all(sk)
+    for i, j in [(0, 0), (3, 7), (5, 2)]:
+        idx = eval_bucket(h.h1[0], i) ^ eval_bucket(h.h2[0], j)
+        noise = sum(eval_sign(h.s1[0], i2) * eval_sign(h.s2[0], j2) * truth[i2, j2]
+                    for i2 in range(n) for j2 in range(n)
+                    if (i2, j2) != (i, j) and (eval_bucket(h.h1[0], i2) ^ eval_bucket(h.h2[0], j2)) == idx)
+        expect = truth[i, j] + eval_sign(h.s1[0], i) * eval_sign(h.s2[0], j) * noise
+        assert abs(est[i, j] - expect) < 1e-9
+        assert est[i, j] == P.decompress_entry(sk, i, j)
+
+
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+def test_single_sketch_estimates_unbiased(transform):
+    n, b, trials = 4, 16, 4000
+    a, m = _pair(np.random.default_rng(7), n)
+    truth = a @ m
+    p = P.SketchParams(n=n, b=b, d=1, transform=transform, seed=0)
+    sketches = P.compress_seeds(a, m, p, range(trials))
+    entries = [(0, 0), (1, 3), (2, 2), (3, 1)]
+    vals = np.array([[P.decompress_entry(sk, i, j) for (i, j) in entries] for sk in sketches])
+    mean, sd = vals.mean(axis=0), vals.std(axis=0)
+    for q, (i, j) in enumerate(entries):
+        assert abs(mean[q] - truth[i, j]) < 4.0 * sd[q] / np.sqrt(trials)
+
+
+def test_variance_within_bound():
+    n, b, trials = 8, 32, 3000
+    a, m = _pair(np.random.default_rng(8), n)
+    truth = a @ m
+    p = P.SketchParams(n=n, b=b, d=1, transform="fwht", seed=0)
+    vals = np.array([P.decompress_entry(sk, 2, 5) for sk in P.compress_seeds(a, m, p, range(trials))])
+    assert np.var(vals, ddof=1) <= 1.3 * float(np.sum(truth * truth)) / b
+
+
+# ---- one-shot transforms (reference test_transforms.py: closed forms, involution,
+# Parseval, convolutions against brute force, FFT against numpy)
+@pytest.mark.parametrize("n", [2, 16, 1024, 1 << 16])
+def test_fwht_involution_and_parseval(n):
+    from paper_2601_09477_b200 import transforms as T
+
+    x = np.random.default_rng(n).normal(size=n)
+    y = T.fwht_inplace(x.copy())
+    assert abs(float(np.dot(y, y)) - n * float(np.dot(x, x))) <= 1e-9 * n * float(np.dot(x, x))
+    z = T.fwht_inplace(y.copy()) / n
+    assert np.max(np.abs(z - x)) <= 1e-12 * max(1.0, np.abs(x).max())
+
+
+@pytest.mark.parametrize("n", [2, 8, 64])
+def test_fwht_matches_dense_hadamard(n):
+    from paper_2601_09477_b200 import transforms as T
+
+    i = np.arange(n)
+    h = (1 - 2 * (np.vectorize(lambda v: bin(v).count("1"))(i[:, None] & i[None, :]) & 1)).astype(np.float64)
+    x = np.random.default_rng(1).normal(size=n)
+    assert np.max(np.abs(T.fwht_inplace(x.copy()) - h @ x)) <= 1e-12 * n
+
+
+@pytest.mark.parametrize("n", [4, 32, 256])
+def test_convolutions_match_brute_force(n):
+    from paper_2601_09477_b200 import transforms as T
+
+    rng = np.random.default_rng(n + 3)
+    x, y = rng.normal(size=n), rng.normal(size=n)
+    xor_ref = np.array([sum(x[i] * y[i ^ w] for i in range(n)) for w in range(n)])
+    cyc_ref = np.array([sum(x[i] * y[(w - i) % n] for i in range(n)) for w in range(n)])
+    assert np.max(np.abs(T.xor_convolve(x, y) - xor_ref)) <= 1e-10 * n
+    assert np.max(np.abs(T.cyclic_convolve(x, y) - cyc_ref)) <= 1e-10 * n
+
+
+@pytest.mark.parametrize("n", [2, 64, 4096])
+def test_fft_forward_matches_numpy_and_inverts(n):
+    from paper_2601_09477_b200 import transforms as T
+
+    x = np.random.default_rng(n + 5).normal(size=n)
+    spec = T.fft_forward(x)
+    assert np.max(np.abs(spec - np.fft.rfft(x))) <= 1e-10 * n
+    assert np.max(np.abs(T.fft_inverse(spec) - x)) <= 1e-12 * max(1.0, np.abs(x).max()) * np.log2(n)
