@@ -209,10 +209,19 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N-rank path on a one-GPU box only (never a measurement):
+    # SMM_BENCH_SAME_DEVICE=1 puts every rank on cuda:0, SMM_BENCH_BACKEND=gloo avoids
+    # NCCL's one-rank-per-device rule
+    if os.environ.get("SMM_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SMM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lib = _lib.load()
 
     w = W.make(args.config, xp=torch, device=dev)
