@@ -364,8 +364,8 @@ def test_two_pass_fft_against_oracle(log2b, n1, m, n2, d):
 @pytest.mark.parametrize("log2b,n1,m,n2,d", [(8, 3000, 70, 2000, 3), (10, 5000, 96, 4000, 5), (12, 9000, 45, 8000, 3),
                                              (14, 1000, 1, 900, 9), (16, 700, 33, 650, 3), (17, 400, 31, 350, 3),
                                              (20, 300, 37, 280, 3),
-                                             # even inner ranges: the pair mapping (b >= 2^13)
-                                             (13, 20000, 30, 300, 3), (13, 700, 34, 650, 3), (14, 3000, 62, 2000, 5),
+                                             # even inner ranges: the pair mapping (b >= 2^12)
+                                             (12, 9000, 46, 8000, 3), (13, 20000, 30, 300, 3), (13, 700, 34, 650, 3), (14, 3000, 62, 2000, 5),
                                              (15, 500, 2, 450, 3), (16, 900, 46, 700, 3), (18, 400, 34, 350, 3)])
 def test_two_pass_fwht_against_oracle(log2b, n1, m, n2, d):
     # fwht2p across its whole range: dense pulls (n >> b: hundreds of CSR entries per warp,
@@ -427,7 +427,7 @@ from paper_2601_09477_b200 import _device
 from oracle import sketch_oracle as O
 rng = np.random.default_rng(5)
 out = []
-for log2b, n in ((13, 700), (14, 1024), (15, 600), (16, 1500), (17, 900)):
+for log2b, n in ((12, 3000), (13, 700), (14, 1024), (15, 600), (16, 1500), (17, 900)):
     a = torch.as_tensor(rng.standard_normal((n, 256)), device="cuda")
     bt = torch.as_tensor(rng.standard_normal((n + 8, 256)), device="cuda")
     words = O.draw_words(31 + log2b, 3, 1 << log2b)
