@@ -16,7 +16,7 @@
 // operand's pass-2 result in TMEM until the product, sums FA*FB over the 32
 // lanes and adds it to the d x b accumulator once per k-tile.  b > 2^16 is
 // folded into F = b / 2^16 slices (one sign per entry).
-// Slices of 2^12..2^16 buckets use the *pair mapping* when the operands allow
+// Slices of 2^8..2^16 buckets use the *pair mapping* when the operands allow
 // 16-byte rows (see "pair mapping" below): lanes own inner-index pairs, 4 + 4
 // bucket bits per pass, bit-identical results with half the memory instructions.
 //
@@ -725,8 +725,8 @@ __device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t,
 
 // Pass 2 of slice s, pair mapping: slice position pi (8 bits) is bucket
 // (pi & hmask) * 256 + lo0 + (pi >> hb); the hb low bits of pi are transformed
-// (4 <= hb <= 8: phase A bits 0-3, phase B bits 4..hb-1; at hb = 4 the exchange only
-// permutes, which still measured 11 % faster than the one-k-per-lane mapping).
+// (phase A bits 0..min(hb, 4)-1, phase B bits 4..hb-1; at hb <= 4 the exchange only
+// permutes, which still measured 11 % faster than the one-k-per-lane mapping at hb = 4).
 template <int HB>
 __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s,
                                          uint32_t tmem, const int *acc_flag, double2 *S) {
@@ -753,7 +753,7 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
       tp::ld2_hint(Ys + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
     }
     PROF_MARK(8);
-    reg_fwht16x2(v);  // eta bits 0-3
+    reg_fwht16x2(v, HB < 4 ? HB : 4);  // pi bits 0..min(hb, 4)-1
     // last use of these Y rows (all read by this warp): drop the L2 lines without write-back
     __syncwarp();
     {
@@ -1161,7 +1161,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   const int G = 2 * num_sms();
   // pair mapping: 16-byte operand rows need an even k origin, stride and range and an aligned base
   static const bool pair_off = getenv("SMM_NO_PAIR") != nullptr;
-  const bool pair = !pair_off && p.hb >= 4 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
+  const bool pair = !pair_off && p.hb >= 0 && (k0 % 2) == 0 && (K % 2) == 0 && (lda % 2) == 0 && (ldb % 2) == 0 &&
                     ((uintptr_t)xa % 16) == 0 && ((uintptr_t)xb % 16) == 0;
   KernelTimer timer(0, s);
   if (pair) switch (p.hb) {
@@ -1171,7 +1171,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
                  "fwht2p smem");                                                                                \
     fwht2p_kernel<H, true><<<G, P_THREADS, smem, s>>>(p);                                                       \
     break;
-    SMM_LAUNCH_PAIR(4) SMM_LAUNCH_PAIR(5) SMM_LAUNCH_PAIR(6) SMM_LAUNCH_PAIR(7) SMM_LAUNCH_PAIR(8)
+    SMM_LAUNCH_PAIR(0) SMM_LAUNCH_PAIR(1) SMM_LAUNCH_PAIR(2) SMM_LAUNCH_PAIR(3) SMM_LAUNCH_PAIR(4) SMM_LAUNCH_PAIR(5) SMM_LAUNCH_PAIR(6) SMM_LAUNCH_PAIR(7) SMM_LAUNCH_PAIR(8)
 #undef SMM_LAUNCH_PAIR
     default: break;
   } else switch (p.hb) {

@@ -427,7 +427,7 @@ from paper_2601_09477_b200 import _device
 from oracle import sketch_oracle as O
 rng = np.random.default_rng(5)
 out = []
-for log2b, n in ((12, 3000), (13, 700), (14, 1024), (15, 600), (16, 1500), (17, 900)):
+for log2b, n in ((8, 500), (10, 2000), (12, 3000), (13, 700), (14, 1024), (15, 600), (16, 1500), (17, 900)):
     a = torch.as_tensor(rng.standard_normal((n, 256)), device="cuda")
     bt = torch.as_tensor(rng.standard_normal((n + 8, 256)), device="cuda")
     words = O.draw_words(31 + log2b, 3, 1 << log2b)
