@@ -36,6 +36,10 @@ struct KernelTimer {
   ~KernelTimer();  // an unstopped timer (error path) returns its events unrecorded
   void stop();
 };
+// The L2 cache-policy encodings of createpolicy.fractional evict_last / evict_first,
+// computed once per device; the two-pass kernels take them as parameters, so their
+// cache-hinted loads and stores read the policy from a uniform register.
+int l2_policies(uint64_t &evict_last, uint64_t &evict_first);
 void kernel_timing(int on);
 int kernel_timing_read(int channel, double *total_ms, int64_t *count);
 

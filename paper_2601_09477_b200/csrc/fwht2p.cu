@@ -182,6 +182,7 @@ struct TwoPassArgs {
   int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
   long long *prof;  // [16] phase cycles (nullable)
   int acc_add;      // add to acc (continue an earlier call's k order) instead of overwriting it
+  uint64_t pol_last, pol_first;  // L2 cache policies (l2_policies)
   int lag;          // pipeline depth in units (nslot = lag + 2)
 };
 
@@ -234,17 +235,8 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // L2 cache-policy hints: Y (the pass-1 -> pass-2 intermediate) is written
-// evict_last so it survives in L2 until pass 2, and read evict_first (last use).
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
+// evict_last so it survives in L2 until pass 2, and read evict_first (last use);
+// the policy operands come from the kernel parameters (TwoPassArgs::pol_*).
 __device__ __forceinline__ void st_hint(double *p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
@@ -388,7 +380,7 @@ __device__ __forceinline__ void p1_operand(const TwoPassArgs &p, int kappa, int 
   // the other operand's first gathers go out before this operand's 64 KB of Y stores
   if (next) gather_first(p, kappa, 1, *next, xpre);
   double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 256) * KT + lane;
-  const uint64_t pol = policy_evict_last();
+  const uint64_t pol = p.pol_last;
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     const int bl = (warp + 8 * (r >> 3)) + 32 * (r & 7);
@@ -430,7 +422,7 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   const uint32_t tq = tmem + ((uint32_t)(32 * wq) << 16);
   const uint32_t col_fa = (uint32_t)(wh * 64);
   double v[32];
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = p.pol_first;
   if constexpr (HB > 5) {
     // Operand 0 goes through the shared-memory exchange and into TMEM in chunks of
     // 8 registers, so operand 1's 32 row loads can already fly during that half.
@@ -706,7 +698,7 @@ __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int
   PROF_MARK(6);
   if (next) gather_first2(p, kappa, 1, *next, xpre);
   double *Yd = p.Y + (((int64_t)slot * 2 + op) * p.bsz + (int64_t)blk * 256) * KT + 2 * kp;
-  const uint64_t pol = policy_evict_last();
+  const uint64_t pol = p.pol_last;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int beta = warp | (lb << 3) | (j << 4);
@@ -742,7 +734,7 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
   const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
   const uint32_t col_fa = (uint32_t)((warp >> 2) * 64);
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = p.pol_first;
   double2 *cell = S + (warp * 32 + lb * 16) * 16 + kp;  // phase-A cells of this lane (j * 16 apart)
   double2 v[16];
 #pragma unroll 1
@@ -1148,6 +1140,10 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.prof = nullptr;
   p.acc_add = acc_add ? 1 : 0;
   p.lag = lag;
+  {
+    const int rc = l2_policies(p.pol_last, p.pol_first);
+    if (rc) return rc;
+  }
   static const bool prof_on = getenv("SMM_PROFILE") != nullptr;
   if (prof_on) {
     cudaMalloc((void **)&p.prof, 16 * sizeof(long long));

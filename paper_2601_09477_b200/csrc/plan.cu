@@ -91,6 +91,36 @@ int kernel_timing_read(int channel, double *total_ms, int64_t *count) {
   return SMM_OK;
 }
 
+__global__ void l2_policy_kernel(uint64_t *out) {
+  uint64_t a, b;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(a));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(b));
+  out[0] = a;
+  out[1] = b;
+}
+
+int l2_policies(uint64_t &evict_last, uint64_t &evict_first) {
+  static uint64_t cache[64][2];
+  static std::atomic<int> have[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!have[dev].load(std::memory_order_acquire)) {  // concurrent first calls compute the same values
+    uint64_t *d = nullptr, h[2];
+    SMM_CUDA_TRY(cudaMalloc(&d, 16), "policy alloc");
+    l2_policy_kernel<<<1, 1>>>(d);
+    const cudaError_t e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    SMM_CUDA_TRY(e, "policy readback");
+    cache[dev][0] = h[0];
+    cache[dev][1] = h[1];
+    have[dev].store(1, std::memory_order_release);
+  }
+  evict_last = cache[dev][0];
+  evict_first = cache[dev][1];
+  return SMM_OK;
+}
+
 int num_sms() {
   static std::atomic<int> cached[64];  // per-device attribute cache (idempotent fill)
   int dev = 0;
