@@ -161,16 +161,19 @@ def stream_chunk(m: int, n_max: int) -> int:
 
 
 def _slab_bounds(m: int, kc: int) -> list:
-    """k-slabs of width kc, the last one split into kc/2, kc/4, kc/4 (multiples of 32):
-    uploads outpace nothing, so after the final upload only the last slab's compute
-    remains exposed — keep it small."""
+    """k-slabs of width kc, the last one split geometrically (kc/2, kc/4, kc/8, kc/8;
+    multiples of 32): uploads outpace nothing, so after the final upload only the last
+    piece's compute remains exposed — keep it small."""
     bounds = [(c0, min(m, c0 + kc)) for c0 in range(0, m, kc)]
     c0, c1 = bounds[-1]
     w = c1 - c0
     if len(bounds) > 1 and w >= 128:
-        h = ((w // 2 + 31) // 32) * 32
-        q = ((w // 4 + 31) // 32) * 32
-        cuts = [c0, c0 + h, min(c1, c0 + h + q), c1]
+        cuts = [c0]
+        for frac in (2, 4, 8):
+            step = ((w // frac + 31) // 32) * 32
+            if cuts[-1] + step < c1:
+                cuts.append(cuts[-1] + step)
+        cuts.append(c1)
         bounds = bounds[:-1] + [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
     return bounds
 
