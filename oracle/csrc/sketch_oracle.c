@@ -327,8 +327,10 @@ int oracle_decompress(const double *polys, int d, int64_t b, int xor_combine,
         v *= s2[(int64_t)t * n2 + j];
         vals[t] = v;
       }
+      int has_nan = 0;
+      for (int t = 0; t < d; ++t) has_nan |= isnan(vals[t]);
       qsort(vals, (size_t)d, sizeof(double), cmp_double);
-      double e = vals[(d - 1) / 2];
+      double e = has_nan ? NAN : vals[(d - 1) / 2];  /* np.median: any NaN gives NaN */
       if (est_out) est_out[r * n2 + j] = e;
       double ae = fabs(e);
       if (strict ? (ae > thr) : (ae >= thr)) cnt++;

@@ -106,6 +106,11 @@ __global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
           v[g][t] *= s2[t];
         }
       }
+      // np.median semantics (sketch.py:398): any NaN among the d values gives NaN
+      bool has_nan = false;
+#pragma unroll
+      for (int t = 0; t < DM; ++t)
+        if (t < d) has_nan |= isnan(v[g][t]);
       double e;
       if (D > 0) {
         e = median_sorted<DM>(v[g]);
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
         }
         e = v[g][(d - 1) / 2];
       }
+      if (has_nan) e = __longlong_as_double(0x7ff8000000000000ll);
       if (colok && p.est) p.est[(i - p.r0) * p.ld_est + j] = e;
       const double ae = fabs(e);
       const bool hit = colok && (p.strict ? (ae > p.thr) : (ae >= p.thr));
@@ -211,13 +217,15 @@ __global__ void query_kernel(SketchHashes h, const double *polys, const int64_t 
       v[t] = x;
       if (reps) reps[q * d + t] = x;
     }
+    bool has_nan = false;
+    for (int t = 0; t < d; ++t) has_nan |= isnan(v[t]);
     for (int a2 = 1; a2 < d; ++a2) {  // insertion sort: the exact middle order statistic
       const double key = v[a2];
       int k = a2 - 1;
       while (k >= 0 && v[k] > key) { v[k + 1] = v[k]; --k; }
       v[k + 1] = key;
     }
-    est[q] = v[(d - 1) / 2];
+    est[q] = has_nan ? __longlong_as_double(0x7ff8000000000000ll) : v[(d - 1) / 2];  // np.median: NaN in, NaN out
   }
 }
 

@@ -153,3 +153,28 @@ def test_fft_forward_matches_numpy_and_inverts(n):
     spec = T.fft_forward(x)
     assert np.max(np.abs(spec - np.fft.rfft(x))) <= 1e-10 * n
     assert np.max(np.abs(T.fft_inverse(spec) - x)) <= 1e-12 * max(1.0, np.abs(x).max()) * np.log2(n)
+
+
+def test_nan_propagates_like_np_median():
+    # reference decompress_all takes np.median over the d values (sketch.py:398): one NaN
+    # among them gives NaN; the threshold never selects a NaN estimate
+    n, b, d = 64, 256, 5
+    a, m = _pair(np.random.default_rng(12), n)
+    p = P.SketchParams(n=n, b=b, d=d, transform="fwht", seed=9)
+    sk = P.compress(a, m, p)
+    polys = sk.polys.copy()
+    polys[2, 17] = np.nan  # one bucket of one repetition
+    sk2 = P.ProductSketch(polys, sk.hashes, p, n, n)
+    est = P.decompress_all(sk2)
+    want = np.array([[np.median(P.sketch_estimates(sk2, i, j)) for j in range(n)] for i in range(n)])
+    assert np.array_equal(np.isnan(est), np.isnan(want)) and np.isnan(est).any() and not np.isnan(est).all()
+    ok = ~np.isnan(want)
+    assert np.array_equal(est[ok], want[ok])
+    q = P.decompress_entries(sk2, np.argwhere(np.isnan(want))[:10])
+    assert np.isnan(q).all()
+    hh = P.heavy_hitters(sk2, 0.0, strict=True)
+    assert not np.isnan(est[hh[:, 0], hh[:, 1]]).any()
+    # a NaN operand entry reaches every repetition: every estimate is NaN, no heavy hitters
+    a[3, 5] = np.nan
+    est = P.decompress_all(P.compress(a, m, p))
+    assert np.isnan(est).all()

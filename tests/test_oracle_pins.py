@@ -99,3 +99,19 @@ def test_accumulate_is_additive_over_k_ranges():
     polys = O.fwht_inverse_scaled(full)
     ref = O.compress(a, bm, b=b, d=d, transform="fwht", seed=5, threads=1)
     assert np.array_equal(polys, ref)
+
+
+def test_oracle_median_propagates_nan_like_numpy():
+    # sketch.py:398 takes np.median over the d values: one NaN among them gives NaN
+    n, b, d = 16, 32, 3
+    words = O.draw_words(4, d, b)
+    polys = np.random.default_rng(1).normal(size=(d, b))
+    polys[1, 7] = np.nan
+    est, cnt, _ = O.decompress(polys, words, b=b, d=d, transform="fwht", n1=n, n2=n, thr=0.0, strict=True)
+    h1, s1, h2, s2 = O.tables(words, d, b, n, n)
+    vals = np.stack([polys[t][h1[t][:, None] ^ h2[t][None, :]] * s1[t][:, None] * s2[t][None, :] for t in range(d)])
+    want = np.median(vals, axis=0)
+    assert np.array_equal(np.isnan(est), np.isnan(want)) and np.isnan(est).any()
+    ok = ~np.isnan(want)
+    assert np.array_equal(est[ok], want[ok])
+    assert int(cnt) == int(np.sum(np.abs(want[ok]) > 0.0))
