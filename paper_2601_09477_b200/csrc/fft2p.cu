@@ -109,6 +109,7 @@ struct Args {
   double *acc;        // [d][b/2 + 1][2]
   int *ctr;           // [0] ticket | done1[U] | done2[U] | acc_cnt[d * NPU * G2]
   int acc_add;
+  int acc_slow;  // test knob (SMM_ACC_SLOWPATH): every P2 item takes the accumulator slow path
 };
 
 // CSR range of one warp's 16 tile positions of operand OP and its first 32 entry
@@ -364,8 +365,11 @@ __device__ __forceinline__ void split_product(double a, double b, double &c, dou
 //     j = i2 - N2/2 - 1 and N2 - 1 - j;
 //   unit pu > 0: row i2 of slice pu with row N2 - 1 - i2 of slice F - pu (the second half).
 // The partner row is transformed in the complement layout, so Z[-u] is register-local.
+// acc_ready (block-uniform): the scheduler thread already acquired this item's accumulator
+// counter (the previous k-tile's update is visible); otherwise the update waits at the end.
 __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu, int slot, int i2, uint32_t tmem,
-                                        const int *acc_flag, double *S) {
+                                        const int *acc_flag, int acc_ready, double *S) {
+  acc_ready |= kappa == 0;  // k-tile 0 adds to a previous launch's accumulator (stream order)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N2 = p.N2, F = p.F;
   bool pair = true;
@@ -386,7 +390,6 @@ __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu,
     halfB = 1;
     baseB = F - pu;
   }
-  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
   // after the lane reduction this lane owns double `lane` = (register lane >> 1, re/im lane & 1)
   const int u1 = post_pos(warp, lane >> 1);
   int entry = -1;
@@ -400,7 +403,6 @@ __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu,
     entry = F * (i2 + N2 * u1);
   }
   double *a = entry >= 0 ? p.acc + (((int64_t)t * (p.bfull / 2 + 1) + entry) * 2 + (lane & 1)) : nullptr;
-  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = (a && (kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   double v[32];
   slice_dft<false>(p, slot, halfA, rowA, v, S);
@@ -451,12 +453,9 @@ __device__ __forceinline__ void p2_item(const Args &p, int kappa, int t, int pu,
       __stcg(a, acc_old + sum);
     }
   }
-  if (kappa > 0 && !acc_ready) {
+  if (kappa > 0 && !acc_ready) {  // slow path: lane 0 acquires, __syncwarp orders the warp after it
     if (lane == 0)
-      while (flag < kappa) {
-        __nanosleep(32);
-        flag = ld_relaxed(acc_flag);
-      }
+      while (ld_acquire(acc_flag) < kappa) __nanosleep(32);
     __syncwarp();
     if (a) __stcg(a, __ldcg(a) + sum);
   }
@@ -511,46 +510,70 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
   int *done2 = done1 + p.U;
   int *acc_cnt = done2 + p.U;
   const int64_t total = (int64_t)p.U * (p.G1 + p.G2);
-  // thread 0 schedules one item ahead (as fwht2p): the next ticket and the next
-  // item's dependency counter are fetched while the current item computes
-  int64_t nxt = 0;
-  Item itn;
-  const int *dep_ptr = nullptr;
-  int dep_target = 0, dep_val = 0;
-  int ver1 = -1, ver2 = -1;
-  auto probe = [&](const Item &it) {
-    dep_ptr = nullptr;
+  // Thread 0 schedules one item ahead (the ticket after next is claimed while the
+  // current item computes).  Dependencies, as fwht2p: thread 32 issues RELAXED loads
+  // of the next item's counters right before [B]; after [B] its fence.acq_rel releases
+  // this item (the completion adds) and acquires those counters; an incomplete
+  // must-precede counter is polled there with ld.acquire; [A] orders the whole CTA.
+  // The accumulator counter (previous k-tile's P2 of the same rows) is only recorded:
+  // if incomplete, the P2 item waits for it per warp at its end (acc_ready).
+  __shared__ int64_t sh_nxt;
+  __shared__ Item sh_itn;
+  __shared__ int sh_ver[2];  // highest unit thread 32 acquired: done1 (P2 items), done2 (P1 slot reuse)
+  __shared__ int s_acc_ok;
+  int64_t &nxt = sh_nxt;
+  Item &itn = sh_itn;
+  struct Deps {
+    const int *ptr[2];
+    int tgt[2], val[2];
+    int ver[2];
+  };
+  auto deps_of = [&](const Item &it, Deps &D) {
+    D.ptr[0] = D.ptr[1] = nullptr;
+    D.tgt[0] = D.tgt[1] = D.val[0] = D.val[1] = 0;
+    D.ver[0] = sh_ver[0];
+    D.ver[1] = sh_ver[1];
     if (it.pos >= total) return;
     if (it.is_p1) {
       const int need = it.u - p.nslot;
-      if (need > ver2) { dep_ptr = done2 + need; dep_target = p.G2; }
-    } else if (it.u > ver1) {
-      dep_ptr = done1 + it.u;
-      dep_target = p.G1;
+      if (need > sh_ver[1]) { D.ptr[0] = done2 + need; D.tgt[0] = p.G2; D.ver[1] = need; }
+    } else {
+      if (it.u > sh_ver[0]) { D.ptr[0] = done1 + it.u; D.tgt[0] = p.G1; D.ver[0] = it.u; }
+      const int kap = fdiv(it.u, p.div_dnpu);
+      if (kap > 0) {
+        const int rem = it.u - kap * p.d * p.NPU;
+        const int tt = fdiv(rem, p.div_npu);
+        D.ptr[1] = acc_cnt + (tt * p.NPU + (rem - tt * p.NPU)) * p.G2 + it.idx;
+        D.tgt[1] = kap;
+      }
     }
-    if (dep_ptr) dep_val = ld_acquire(dep_ptr);
+  };
+  auto deps_settle = [&](Deps &D) {
+    if (D.ptr[0] && D.val[0] < D.tgt[0])
+      while (ld_acquire(D.ptr[0]) < D.tgt[0]) __nanosleep(32);
+    sh_ver[0] = D.ver[0];
+    sh_ver[1] = D.ver[1];
+    s_acc_ok = (!D.ptr[1] || D.val[1] >= D.tgt[1]) ? 1 : 0;
   };
   if (tid == 0) {
     const int64_t cur = atomicAdd(ticket, 1);
     nxt = atomicAdd(ticket, 1);
     itn = decode_item(p, cur);
-    probe(itn);
+    sh_ver[0] = sh_ver[1] = -1;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 32) {  // the first item's dependencies
+    Deps D;
+    deps_of(itn, D);
+    deps_settle(D);
+    s_acc_ok = 0;
+  }
   const uint32_t tmem = s_tmem;
   while (true) {
     if (tid == 0) {
       const Item it = itn;
-      if (dep_ptr) {  // dispensed earlier than this item: cannot deadlock
-        while (dep_val < dep_target) {
-          __nanosleep(64);
-          dep_val = ld_acquire(dep_ptr);
-        }
-        if (it.is_p1) ver2 = it.u - p.nslot;
-        else ver1 = it.u;
-      }
       s_item[0] = it.pos < total ? 1 : 0;
       s_item[1] = it.is_p1;
       s_item[2] = it.u;
@@ -570,23 +593,31 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
     const int go = s_item[0];
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
     const int kappa = s_item[4], t = s_item[5], slot = s_item[6], pu = s_item[7];
-    if (tid == 0 && go) {
-      probe(itn);
-      nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
-    }
+    const int acc_ok = s_acc_ok && !p.acc_slow;
+    if (tid == 0 && go) nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
     if (!go) break;
+    int *acc_flag = acc_cnt + (t * p.NPU + pu) * p.G2 + idx;
     if (is_p1) p1_item<S1, FOLD>(p, kappa, t, pu, slot, idx, S);
-    else p2_item(p, kappa, t, pu, slot, idx, tmem, acc_cnt + (t * p.NPU + pu) * p.G2 + idx, S);
+    else p2_item(p, kappa, t, pu, slot, idx, tmem, acc_flag, acc_ok, S);
+    Deps D;  // thread 32: relaxed probe of the next item's counters (acquired by the fence below)
+    if (tid == 32) {
+      const Item nx = itn;
+      deps_of(nx, D);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (D.ptr[j]) D.val[j] = ld_relaxed(D.ptr[j]);
+    }
     tc_fence_before();
     __syncthreads();  // [B]
     tc_fence_after();
-    if (tid == 32) {  // publish (release covers the CTA's writes through [B])
+    if (tid == 32) {  // release this item (covered through [B]); acquire the probed counters
       fence_acq_rel();
       if (is_p1) red_add(done1 + u, 1);
       else {
-        red_add(acc_cnt + (t * p.NPU + pu) * p.G2 + idx, 1);
+        red_add(acc_flag, 1);
         red_add(done2 + u, 1);
       }
+      deps_settle(D);
     }
   }
   tc_fence_before();
@@ -784,6 +815,8 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   p.acc = acc;
   p.ctr = ctr;
   p.acc_add = acc_add ? 1 : 0;
+  static const bool acc_slow = getenv("SMM_ACC_SLOWPATH") != nullptr;
+  p.acc_slow = acc_slow ? 1 : 0;
   const size_t smem = (size_t)8 * 32 * 32 * 8;
   const int G = 2 * num_sms();
 #define F2P_LAUNCH(SS, FD)                                                                             \

@@ -179,18 +179,13 @@ struct TwoPassArgs {
   int64_t nmax, bsz;
   double *Y;   // [nslot][2][b][KT]
   double *acc; // [d][b]
-  int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * nblk]
+  int *ctr;    // [0] ticket | done1[U] | done2[U] | acc_cnt[d * F * nblk]
   long long *prof;  // [16] phase cycles (nullable)
   int acc_add;      // add to acc (continue an earlier call's k order) instead of overwriting it
   uint64_t pol_last, pol_first;  // L2 cache policies (l2_policies)
   int lag;          // pipeline depth in units (nslot = lag + 2)
+  int acc_slow;     // test knob (SMM_ACC_SLOWPATH): every P2 item takes the accumulator slow path
 };
-
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ int ld_relaxed(const int *p) {
   int v;
@@ -198,9 +193,10 @@ __device__ __forceinline__ int ld_relaxed(const int *p) {
   return v;
 }
 
-__device__ __forceinline__ void wait_geq(const int *p, int target) {
-  if (ld_acquire(p) >= target) return;
-  while (ld_acquire(p) < target) __nanosleep(64);
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // ---- TMEM helpers (32x32b shape: thread <-> TMEM lane, 16 x 32-bit columns = 8 doubles)
@@ -404,10 +400,11 @@ __device__ __forceinline__ void p1_item(const TwoPassArgs &p, int kappa, int t, 
 // registers <- sigma 0-4, warp <- sigma 5-7; bucket = hi * 256 + lo.
 template <int HB>
 __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s, uint32_t tmem,
-                                        const int *acc_flag, double *S) {
+                                        const int *acc_flag, int acc_ready, double *S) {
+  acc_ready |= kappa == 0;  // k-tile 0 adds to a previous launch's accumulator (stream order)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // the accumulator of (t, s) must already hold k-tiles < kappa: poll early, check before the update
-  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
+  // acc_ready (block-uniform): the scheduler already acquired the slice's counter, i.e. the
+  // accumulator holds k-tiles < kappa; otherwise the update waits at the end (slow path)
   const int wq = warp & 3, wh = warp >> 2;
   constexpr int hb = HB;
   const int hmask = (1 << hb) - 1;
@@ -417,7 +414,6 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   const int sg_acc = hb > 5 ? ((rl & 3) | (warp << 2) | ((rl >> 2) << 5)) : (rl | (warp << 5));
   double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + (int64_t)(sg_acc & hmask) * 256 + lo0 + (sg_acc >> hb);
   // usually the previous k-tile's update of this slice finished long ago: fetch the old value early
-  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * wq) << 16);
   const uint32_t col_fa = (uint32_t)(wh * 64);
@@ -546,11 +542,10 @@ __device__ __forceinline__ void p2_item(const TwoPassArgs &p, int kappa, int t, 
   } else if (acc_ready) {
     __stcg(a, acc_old + sum);
   } else {
+    // slow path: lane 0 acquires the counter, __syncwarp orders the warp's loads after it
+    // (a CTA barrier here measured 15 % slower on cfg3)
     if (lane == 0)
-      while (flag < kappa) {
-        __nanosleep(32);
-        flag = ld_relaxed(acc_flag);
-      }
+      while (ld_acquire(acc_flag) < kappa) __nanosleep(32);
     __syncwarp();
     __stcg(a, __ldcg(a) + sum);
   }
@@ -721,16 +716,15 @@ __device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t,
 // permutes, which still measured 11 % faster than the one-k-per-lane mapping at hb = 4).
 template <int HB>
 __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t, int a_sl, int slot, int s,
-                                         uint32_t tmem, const int *acc_flag, double2 *S) {
+                                         uint32_t tmem, const int *acc_flag, int acc_ready, double2 *S) {
+  acc_ready |= kappa == 0;  // k-tile 0 adds to a previous launch's accumulator (stream order)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kp = lane & 15, lb = lane >> 4;
-  int flag = lane == 0 ? ld_relaxed(acc_flag) : 0;
   // after the lane reduction lane (lb, kp) of warp w holds eta = w | lb << 3 | kp << 4
   constexpr int hmask = (1 << HB) - 1;
   const int64_t lo0 = (int64_t)s << (P1_BITS - HB);
   auto row_of = [&](int pi) { return (int64_t)(pi & hmask) * 256 + lo0 + (pi >> HB); };
   double *a = p.acc + ((int64_t)t * p.F + a_sl) * p.bsz + row_of(warp | (lb << 3) | (kp << 4));
-  const bool acc_ready = __shfl_sync(0xffffffffu, flag, 0) >= kappa;
   const double acc_old = ((kappa > 0 || p.acc_add) && acc_ready) ? __ldcg(a) : 0.0;
   const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
   const uint32_t col_fa = (uint32_t)((warp >> 2) * 64);
@@ -788,11 +782,10 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
   } else if (acc_ready) {
     __stcg(a, acc_old + sum);
   } else {
+    // slow path: lane 0 acquires the counter, __syncwarp orders the warp's loads after it
+    // (a CTA barrier here measured 15 % slower on cfg3)
     if (lane == 0)
-      while (flag < kappa) {
-        __nanosleep(32);
-        flag = ld_relaxed(acc_flag);
-      }
+      while (ld_acquire(acc_flag) < kappa) __nanosleep(32);
     __syncwarp();
     __stcg(a, __ldcg(a) + sum);
   }
@@ -850,71 +843,87 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   int *ticket = p.ctr;
   int *done1 = p.ctr + 1;
   int *done2 = done1 + p.U;
-  int *acc_cnt = done2 + p.U;
+  int *acc_cnt = done2 + p.U;  // P2 completions per accumulator slice (t, a, s): k-tiles done
   const int G1 = p.nblk, G2 = p.nblk;  // P1 items: one block, both operands; P2 items: one slice
   const int log2g = 31 - __clz(2 * p.nblk);
   const int64_t total = (int64_t)p.U * (G1 + G2);
-  // Thread 0 runs the scheduler one item ahead: the ticket after next and the
-  // dependency counter of the next item are fetched while the current item
-  // computes.  Thread 32 publishes an item's completion (fence + relaxed adds)
-  // right after the item's closing barrier, concurrently with thread 0's
-  // scheduling, so the fence latency is not serialised with it.  Every warp
-  // prefetches the CSR head of the next pass-1 item during the current item.
-  // scheduler state lives in shared memory: only thread 0 touches it, and as
-  // registers it would cost every thread ~14 of its 128
+  // Scheduling (thread 0) runs one item ahead: the ticket after next is claimed
+  // while the current item computes, and every warp prefetches the CSR heads of
+  // the next pass-1 item.  Dependencies (thread 32): right before the closing
+  // barrier [B] of item i it issues RELAXED loads of the counters that item i+1
+  // depends on (P1(u): every P2 of unit u - nslot, whose Y slot it reuses; P2(u):
+  // every P1 of unit u, and the slice's accumulator counter, i.e. the previous
+  // k-tile's P2 of the same accumulator rows).  After [B] its fence.acq_rel both
+  // releases item i (the completion adds that follow) and turns those loads into
+  // acquires (PTX acquire pattern: relaxed read, then fence); a counter not yet
+  // complete is polled there with ld.acquire.  Barrier [A] then extends the order
+  // to the whole CTA, so every Y / accumulator read of item i+1 happens after its
+  // producers' writes.  Every dependency was dispensed before the item that waits
+  // on it, so waiting cannot deadlock.  Scheduler state lives in shared memory (as
+  // registers it would cost every thread ~14 of its 128).
   __shared__ int64_t sh_nxt;
   __shared__ Item sh_itn;
-  __shared__ const int *sh_dep_ptr;
-  __shared__ int sh_dep_target, sh_dep_val, sh_ver1, sh_ver2;
+  __shared__ int sh_ver[2];  // highest unit whose completion thread 32 acquired: done1 (P2), done2 (P1)
+  __shared__ int s_acc_ok;   // the next P2 item's accumulator counter was acquired complete
   int64_t &nxt = sh_nxt;
   Item &itn = sh_itn;
-  const int *&dep_ptr = sh_dep_ptr;
-  int &dep_target = sh_dep_target, &dep_val = sh_dep_val;
-  int &ver1 = sh_ver1, &ver2 = sh_ver2;  // highest unit whose P1 / P2 completion this CTA has seen
-  if (tid == 0) {
-    nxt = 0;
-    dep_ptr = nullptr;
-    dep_target = dep_val = 0;
-    ver1 = ver2 = -1;
-  }
-  auto probe = [&](const Item &it) {
-    dep_ptr = nullptr;
+  struct Deps {
+    const int *ptr[2];
+    int tgt[2], val[2];
+    int ver[2];
+  };
+  auto deps_of = [&](const Item &it, Deps &D) {
+    D.ptr[0] = D.ptr[1] = nullptr;
+    D.tgt[0] = D.tgt[1] = D.val[0] = D.val[1] = 0;
+    D.ver[0] = sh_ver[0];
+    D.ver[1] = sh_ver[1];
     if (it.pos >= total) return;
     if (it.is_p1) {
       const int need = it.u - p.nslot;
-      if (need > ver2) { dep_ptr = done2 + need; dep_target = G2; }
+      if (need > sh_ver[1]) { D.ptr[0] = done2 + need; D.tgt[0] = G2; D.ver[1] = need; }
     } else {
-      if (it.u > ver1) { dep_ptr = done1 + it.u; dep_target = G1; }
+      if (it.u > sh_ver[0]) { D.ptr[0] = done1 + it.u; D.tgt[0] = G1; D.ver[0] = it.u; }
+      const int kap = fdiv(it.u, p.div_df);
+      if (kap > 0) {
+        const int ut = fmod_(it.u, p.div_df);
+        D.ptr[1] = acc_cnt + (fdiv(ut, p.div_F) * p.F + fmod_(ut, p.div_F)) * p.nblk + it.idx;
+        D.tgt[1] = kap;
+      }
     }
-    if (dep_ptr) dep_val = ld_acquire(dep_ptr);  // issued an item ahead: its latency is hidden
+  };
+  // after the acquire fence (or none): poll the must-precede dependency if incomplete; the
+  // accumulator counter is only recorded — if incomplete the P2 item waits for it at its end
+  auto deps_settle = [&](Deps &D) {
+    if (D.ptr[0] && D.val[0] < D.tgt[0]) {
+      const long long w0 = g_prof_on ? clock64() : 0;
+      while (ld_acquire(D.ptr[0]) < D.tgt[0]) __nanosleep(32);
+      if (g_prof_on) s_prof[11] += clock64() - w0;  // informational
+    }
+    sh_ver[0] = D.ver[0];
+    sh_ver[1] = D.ver[1];
+    s_acc_ok = (!D.ptr[1] || D.val[1] >= D.tgt[1]) ? 1 : 0;
   };
   if (tid == 0) {
     const int64_t cur = atomicAdd(ticket, 1);
     nxt = atomicAdd(ticket, 1);
     itn = decode_item(p, cur, log2g);
-    probe(itn);
+    sh_ver[0] = sh_ver[1] = -1;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 32) {  // the first item's dependencies (usually none)
+    Deps D;
+    deps_of(itn, D);
+    deps_settle(D);
+    s_acc_ok = 0;
+  }
   const uint32_t tmem = s_tmem;
   PullHead hd_next, hd_next1;  // both operands' CSR heads of the next pass-1 item
   bool hd_valid = false;
   while (true) {
     if (tid == 0) {
       const Item it = itn;
-      if (dep_ptr) {  // dependency of this item (dispensed earlier: cannot deadlock)
-        const long long w0 = g_prof_on ? clock64() : 0;
-        while (dep_val < dep_target) {
-          __nanosleep(64);
-          dep_val = ld_acquire(dep_ptr);
-        }
-        if (g_prof_on) s_prof[it.is_p1 ? 11 : 12] += clock64() - w0;  // informational (inside m0)
-        if (it.is_p1) ver2 = it.u - p.nslot;
-        else ver1 = it.u;
-        // the counter was observed with acquire loads; barrier [A] extends the order
-        // to the CTA (a counter already observed by an earlier item needs nothing new)
-      }
       PROF_MARK(13);
       const Item in = decode_item(p, nxt, log2g);
       const int ut = fmod_(it.u, p.div_df);
@@ -941,10 +950,8 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
     const int kappa = s_item[4], t = s_item[5], slot = s_item[6], asl = s_item[10];
     const int next_p1 = s_item[7], next_t = s_item[8], next_idx = s_item[9];
-    if (tid == 0 && go) {
-      probe(itn);
-      nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
-    }
+    const int acc_ok = s_acc_ok && !p.acc_slow;
+    if (tid == 0 && go) nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
     if (!go) break;
     PullHead hd_cur, hd_cur1;
     auto head = [&](int tt, int op, int blk) { return PAIR ? pull_head2(p, tt, op, blk) : pull_head(p, tt, op, blk); };
@@ -960,23 +967,34 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     const int *acc_flag = acc_cnt + (t * p.F + asl) * p.nblk + idx;
     if constexpr (PAIR) {
       if (is_p1) p1_item2(p, kappa, t, asl, slot, idx, (double2 *)S, hd_cur1, hd_cur);
-      else p2_item2<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, (double2 *)S);
+      else p2_item2<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, acc_ok, (double2 *)S);
     } else {
       if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
-      else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, S);
+      else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, acc_ok, S);
+    }
+    // thread 32: relaxed probe of the next item's dependency counters (acquired by the fence below)
+    Deps D;
+    if (tid == 32) {
+      const Item nx = itn;
+      deps_of(nx, D);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (D.ptr[j]) D.val[j] = ld_relaxed(D.ptr[j]);
     }
     tc_fence_before();
     PROF_MARK(2);
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
     PROF_MARK(10);
     tc_fence_after();
-    if (tid == 32) {  // publish this item's completion (release: covers the CTA's writes via [B])
+    if (tid == 32) {
+      // release this item's writes (covered through [B]) and acquire the probed counters
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       if (is_p1) red_add(done1 + u, 1);
       else {
         red_add(acc_cnt + (t * p.F + asl) * p.nblk + idx, 1);
         red_add(done2 + u, 1);
       }
+      deps_settle(D);
     }
   }
   tc_fence_before();
@@ -1140,6 +1158,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.prof = nullptr;
   p.acc_add = acc_add ? 1 : 0;
   p.lag = lag;
+  static const bool acc_slow = getenv("SMM_ACC_SLOWPATH") != nullptr;
+  p.acc_slow = acc_slow ? 1 : 0;
   {
     const int rc = l2_policies(p.pol_last, p.pol_first);
     if (rc) return rc;

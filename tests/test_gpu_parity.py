@@ -458,3 +458,53 @@ def test_pair_mapping_bit_identical_to_one_k_per_lane(tmp_path, _):
     for x, y in zip(res["pair"], res["lane"]):
         assert np.array_equal(x, y)
         assert np.abs(x).max() > 0
+
+
+_SLOW_CASE = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2601_09477_b200 import _device
+from oracle import sketch_oracle as O
+rng = np.random.default_rng(9)
+out = []
+for transform, log2b, n in (("fwht", 12, 700), ("fwht", 16, 900), ("fwht", 17, 500), ("fft", 12, 600),
+                            ("fft", 15, 500)):
+    a = torch.as_tensor(rng.standard_normal((n, 320)), device="cuda")
+    bm = torch.as_tensor(rng.standard_normal((320, n)), device="cuda")
+    words = O.draw_words(7 + log2b, 3, 1 << log2b)
+    acc = _device.compress_accumulate(a, bm, words, 3, log2b, transform, 0, 320, a_layout=_device.KMINOR)
+    out.append(acc.cpu().numpy())
+    # accumulate mode: two calls over [0, 160) and [160, 320) continue one k order
+    acc2 = _device.compress_accumulate(a[:, :160], bm[:160], words, 3, log2b, transform, 0, 160,
+                                       a_layout=_device.KMINOR)
+    _device.compress_accumulate(a[:, 160:], bm[160:], words, 3, log2b, transform, 0, 160, acc=acc2,
+                                a_layout=_device.KMINOR, accumulate=True)
+    out.append(acc2.cpu().numpy())
+np.savez({path!r}, *out)
+"""
+
+
+def test_accumulator_slow_path_bit_identical(tmp_path):
+    """SMM_ACC_SLOWPATH=1 sends every pass-2 item of fwht2p / fft2p through the
+    accumulator slow path (per-warp acquire of the slice counter at the end of the
+    item instead of the scheduler's acquire before it): same k order, so the
+    accumulators must be bit-identical to the default run, in one call and in
+    accumulate mode across two calls."""
+    import os
+    import subprocess
+    import sys
+
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for tag, env in (("fast", {}), ("slow", {"SMM_ACC_SLOWPATH": "1"})):
+        path = str(tmp_path / f"{tag}.npz")
+        subprocess.run([sys.executable, "-c", _SLOW_CASE.format(root=root, path=path)], check=True,
+                       env={**os.environ, **env}, timeout=300)
+        g = np.load(path)
+        res[tag] = [g[f"arr_{i}"] for i in range(len(g.files))]
+    for i, (x, y) in enumerate(zip(res["fast"], res["slow"])):
+        assert np.array_equal(x, y), i
+        assert np.abs(x).max() > 0
+    # one call and two accumulate-mode calls agree as well (FWHT two-pass: bit for bit)
+    for i in (0, 2, 4):
+        assert np.array_equal(res["fast"][i], res["fast"][i + 1]), i
