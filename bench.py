@@ -14,8 +14,14 @@ accumulators are summed with one NCCL allreduce, and output rows are sharded:
 same total work, strong scaling; the reported time is the max over ranks.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
-bit-exact C/OpenMP oracle port, oracle/, all host cores) on a bounded k-slice /
-row-slice sample of the same workload, extrapolated to the full product.
+bit-exact C/OpenMP oracle port, oracle/, all host cores) running the FULL product
+of the same workload every step (A^T copy, compress over all n inner indices,
+inverse, all n^2 estimates, threshold and pair list) — no extrapolation.  When
+the unmodified reference package is installed in baseline/_ref
+(tools/install_reference.sh), one full run of its own Numba path (sketchmm.compress
++ decompress_all + threshold) is added as ``cpu_baseline.detail.stock_reference``.
+Our arm also lists cuBLAS DGEMM (torch.matmul, float64) on the same A, B as
+context (the reference's timing harness does the same, experiments.py:505-516).
 """
 
 from __future__ import annotations
@@ -145,6 +151,60 @@ def _calibrate(w, threads: int, budget_s: float):
     return k_slice, row_slice
 
 
+def _oracle_full(w, threads: int):
+    """One full sketched product on the CPU oracle (the reference's algorithm, bit-exact
+    port): A^T copy (sketch.py:305), compress over every inner index, inverse, all n^2
+    estimates (sketch.py:375-399), threshold and the row-major pair list."""
+    from oracle import sketch_oracle as O
+
+    words = O.draw_words(w.sketch_seed, w.d, w.b)
+    t0 = time.perf_counter()
+    at = np.ascontiguousarray(w.a.T)
+    acc = O.accumulate_fwht(at, w.bmat, b=w.b, d=w.d, words=words, k0=0, k1=w.n, threads=threads)
+    del at
+    t1 = time.perf_counter()
+    polys = O.fwht_inverse_scaled(acc)
+    t2 = time.perf_counter()
+    _, cnt, _ = O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, want_est=True,
+                             thr=w.threshold, strict=True, want_hh=True, threads=threads)
+    t3 = time.perf_counter()
+    return (t3 - t0) * 1e3, {"compress_s": t1 - t0, "inverse_s": t2 - t1, "decompress_threshold_s": t3 - t2,
+                             "heavy_hitters": int(cnt)}
+
+
+def _stock_reference(w):
+    """One full run of the unmodified reference (baseline/_ref, Numba) on the same inputs, or why not."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "sketchmm").exists():
+        return {"unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    sys.path.insert(0, str(ref_dir))
+    try:
+        import numba
+        from sketchmm import sketch as RS
+
+        threads = int(numba.config.NUMBA_NUM_THREADS)
+        # JIT warm-up on a small instance of the same dtypes
+        small = np.ones((64, 64))
+        RS.decompress_all(RS.compress(small, small, RS.SketchParams(n=64, b=1 << 8, d=w.d, seed=1), threads=threads))
+        p = RS.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
+        t0 = time.perf_counter()
+        sk = RS.compress(w.a, w.bmat, p, threads=threads)
+        t1 = time.perf_counter()
+        est = RS.decompress_all(sk)
+        t2 = time.perf_counter()
+        hh = np.argwhere(np.abs(est) > w.threshold)
+        t3 = time.perf_counter()
+        return {"value_ms": (t3 - t0) * 1e3, "compress_s": t1 - t0, "decompress_all_s": t2 - t1,
+                "threshold_s": t3 - t2, "heavy_hitters": int(hh.shape[0]), "threads": threads,
+                "numba": numba.__version__, "note": "unmodified sketchmm from baseline/_ref, one run after a "
+                                                    "small JIT warm-up; informational"}
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:300]}
+    finally:
+        sys.path.remove(str(ref_dir))
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -154,24 +214,24 @@ def run_reference(args) -> None:
     O.build()
     threads = O.cpu_count()
     w = _cpu_instance(args.config)
-    k_slice, row_slice = _calibrate(w, threads, args.ref_step_budget)
     times = []
     info = None
     for step in range(args.warmup + args.steps):
-        ms, info = _oracle_sample(w, k_slice, row_slice, threads)
+        ms, info = _oracle_full(w, threads)
         if step >= args.warmup:
             times.append(ms)
     value = float(np.median(times))
-    sample = (f"oracle C/OpenMP port (bit-exact vs reference Numba kernels): compress k-slice of {k_slice}/{w.n} "
-              f"inner indices + inverse + decompress/threshold of {row_slice}/{w.n} rows, extrapolated linearly "
-              f"to the full n={w.n} product per step")
+    sample = (f"oracle C/OpenMP port (bit-exact vs reference Numba kernels) on {threads} host threads: the full "
+              f"n={w.n} product every step (A^T copy, compress over all inner indices, inverse, all n^2 "
+              f"estimates, threshold + pair list); median of {args.steps} steps")
+    stock = _stock_reference(w) if not args.no_stock_reference else {"unavailable": "--no-stock-reference"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg3 construction)",
             "config": _config(args, w.n, w.b, w.d),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "sample_detail": info}
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "detail": {"last_step": info, "stock_reference": stock}},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -180,6 +240,30 @@ def _config(args, n, b, d):
                         f"entries, heavy-hitter threshold |est|>n/2; compress + inverse + full n^2 extraction + threshold",
             "n": n, "b": b, "d": d, "transform": "fwht", "parallelism": f"k-shard x{args.gpus} + 1 allreduce",
             "l2": "operands (2 x 2 GiB) exceed the 126 MB L2; no flush needed between steps"}
+
+
+TRAFFIC_FILE = ROOT / "profiles" / "compress_dram_bytes.json"
+
+
+def _kernel_source_sha() -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in ("fwht2p.cu", "twopass.cuh", "plan.cuh", "common.cuh"):
+        h.update((ROOT / "paper_2601_09477_b200" / "csrc" / f).read_bytes())
+    return h.hexdigest()[:16]
+
+
+def _traffic():
+    """DRAM bytes per fwht2p launch from the committed ncu --set full capture, used only
+    if that capture was taken of the kernel source built here (sha match); else null."""
+    try:
+        rec = json.loads(TRAFFIC_FILE.read_text())
+    except Exception:  # noqa: BLE001
+        return None, "no ncu capture committed"
+    if rec.get("kernel_source_sha") != _kernel_source_sha():
+        return None, f"stale: {TRAFFIC_FILE.name} was captured from another fwht2p source"
+    return rec.get("dram_bytes_per_launch"), f"{TRAFFIC_FILE.name} ({rec.get('report')})"
 
 
 L2_WRITE_TBS = 7.57  # L2-resident store bandwidth (tools/microbench.cu)
@@ -219,6 +303,10 @@ def run_ours(args) -> None:
     if world > 1:
         backend = os.environ.get("SMM_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator set-up (transport, NVLS) on stderr: the JSON line stays alone on stdout
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -312,12 +400,7 @@ def run_ours(args) -> None:
                 # the pass-1 -> pass-2 intermediate Y crosses L2 once per element and operand:
                 # written at <= 7.57 TB/s and read at <= 17.5 TB/s (measured, profiles/r01_microbench.txt)
                 "l2": _l2_view(kl, b, d, t_comp)}
-    traffic_file = ROOT / "profiles" / "r01_compress_dram_bytes.json"
-    if traffic_file.exists():
-        try:
-            roofline["traffic"] = json.loads(traffic_file.read_text()).get("dram_bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            pass
+    roofline["traffic"], roofline["traffic_source"] = _traffic()
 
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
@@ -357,6 +440,28 @@ def run_ours(args) -> None:
                        "compute) + extract_all(est_out=pinned host rows; row blocks copied out while the next "
                        "extracts; heavy-hitter pairs returned in pinned host memory)"}
 
+    # ---- context only: cuBLAS DGEMM of the same A, B (the dense product the sketch replaces)
+    dgemm = None
+    if not args.no_dgemm:
+        try:
+            c = torch.matmul(a_slab, b_slab)
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            reps = 3
+            for _ in range(reps):
+                c = torch.matmul(a_slab, b_slab)
+            g1.record()
+            torch.cuda.synchronize()
+            gms = g0.elapsed_time(g1) / reps
+            del c
+            dgemm = {"ms": gms, "tflops": 2.0 * n * (k1 - k0) * n / (gms * 1e-3) / 1e12,
+                     "what": "torch.matmul float64 (cuBLAS DGEMM) of this rank's A[:, k-slab] @ B[k-slab, :], "
+                             "n x n output; context only (reference experiments.py:505-516 times the dense "
+                             "product beside the sketch)"}
+        except RuntimeError as exc:  # e.g. out of memory
+            dgemm = {"unavailable": str(exc)[:200]}
+
     # ---- CPU baseline (rank 0, N=1): bounded oracle sample on the host cores
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -379,6 +484,7 @@ def run_ours(args) -> None:
                 "config": _config(args, n, b, d), "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(),
                 "breakdown_ms": {"compress_accumulate": t_comp, "extract_all": t_extract},
+                "context_dgemm": dgemm,
                 "heavy_hitters_rank0": hh_local}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -396,7 +502,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
-    ap.add_argument("--ref-step-budget", type=float, default=4.0, help="seconds per --impl reference step")
+    ap.add_argument("--no-dgemm", action="store_true", help="skip the cuBLAS DGEMM context timing")
+    ap.add_argument("--no-stock-reference", action="store_true",
+                    help="--impl reference: skip the one run of the unmodified reference (baseline/_ref)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -52,7 +52,13 @@ extern "C" {
 #define SMM_VARIANT_FFT 0
 #define SMM_VARIANT_FWHT 1
 
+/* Repetitions per kernel launch (the hash functions travel in the kernel
+ * parameter block).  Deeper sketches (any odd d up to SMM_MAX_DEPTH_TOTAL, the
+ * reference accepts any odd d, sketch.py:75-76) are compressed in groups of
+ * SMM_MAX_DEPTH repetitions and extracted by a kernel that reads the hash
+ * functions from device memory. */
 #define SMM_MAX_DEPTH 63
+#define SMM_MAX_DEPTH_TOTAL 511
 
 /* OR into `variant` of the compress entry points: acc is ADDED to instead of
  * overwritten.  With the two-pass FWHT kernel and k-ranges split on multiples of

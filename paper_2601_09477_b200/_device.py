@@ -75,7 +75,8 @@ def transpose(x: torch.Tensor) -> torch.Tensor:
     lib = _lib.load()
     rows, cols = x.shape
     out = torch.empty((cols, rows), dtype=torch.float64, device=x.device)
-    _lib.check(lib.smm_transpose(ptr(x), rows, cols, x.stride(0), ptr(out), rows, stream_ptr(x.device)))
+    with torch.cuda.device(x.device):
+        _lib.check(lib.smm_transpose(ptr(x), rows, cols, x.stride(0), ptr(out), rows, stream_ptr(x.device)))
     return out
 
 
@@ -117,13 +118,15 @@ def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: 
         v |= _lib.FLAG_ACCUMULATE
     nbytes = ctypes.c_int64(0)
     _lib.check(lib.smm_compress_workspace_ex(v, d, log2b, n1, n2, k0, k1, a_layout, b_layout, ctypes.byref(nbytes)))
-    ws = workspace(nbytes.value, dev)
-    if acc is None:
-        acc = torch.empty(acc_shape(variant, d, 1 << log2b), dtype=torch.float64, device=dev)
-    words, wp = words_ptr(words)
-    _lib.check(lib.smm_compress_accumulate_ex(v, ptr(a), a.stride(0), a_layout, ptr(b), b.stride(0), b_layout, n1,
-                                              n2, k0, k1, wp, d, log2b, ptr(acc), ptr(ws), ws.numel(),
-                                              stream_ptr(dev)))
+    # the library launches on the current device: make it the operands' device
+    with torch.cuda.device(dev):
+        ws = workspace(nbytes.value, dev)
+        if acc is None:
+            acc = torch.empty(acc_shape(variant, d, 1 << log2b), dtype=torch.float64, device=dev)
+        words, wp = words_ptr(words)
+        _lib.check(lib.smm_compress_accumulate_ex(v, ptr(a), a.stride(0), a_layout, ptr(b), b.stride(0), b_layout,
+                                                  n1, n2, k0, k1, wp, d, log2b, ptr(acc), ptr(ws), ws.numel(),
+                                                  stream_ptr(dev)))
     return acc
 
 
@@ -198,6 +201,11 @@ def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, l
         return compress_accumulate(torch.empty((0, n1) if a_layout == KMAJOR else (n1, 0), dtype=torch.float64,
                                                device=device), torch.empty((0, n2), dtype=torch.float64, device=device),
                                    words, d, log2b, variant, 0, 0, acc, a_layout, KMAJOR)
+    with torch.cuda.device(device):
+        return _compress_host(a, b, words, d, log2b, variant, a_layout, device, kc, acc, m, n1, n2)
+
+
+def _compress_host(a, b, words, d, log2b, variant, a_layout, device, kc, acc, m, n1, n2):
     compute = torch.cuda.current_stream(device)
     copy = torch.cuda.Stream(device)
     abuf = [torch.empty((n1, kc) if a_layout == KMINOR else (kc, n1), dtype=torch.float64, device=device)
@@ -221,6 +229,9 @@ def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, l
             copy2d(bbuf[q][:w], b[c0:c1], copy)
             loaded[q].record(copy)
 
+    # the ring buffers come from the compute stream's pool: blocks freed there may still
+    # be in use by queued kernels, so the copy stream starts behind the compute stream
+    copy.wait_stream(compute)
     upload(0)
     for c, (c0, c1) in enumerate(slabs):
         if c + 1 < len(slabs):
@@ -233,6 +244,11 @@ def compress_host(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: int, l
                             accumulate=c > 0)
         freed[q].record(compute)
     compute.wait_stream(copy)
+    # the DMA reads the caller's host tensors asynchronously (pinned memory): return only
+    # once the last upload has finished, so the caller may free or reuse them
+    uploaded = torch.cuda.Event()
+    uploaded.record(copy)
+    uploaded.synchronize()
     return acc
 
 
@@ -252,37 +268,71 @@ def kernel_timing_read(channel: int) -> tuple[float, int]:
 def finalize(acc: torch.Tensor, d: int, log2b: int, variant: str) -> torch.Tensor:
     lib = _lib.load()
     polys = torch.empty((d, 1 << log2b), dtype=torch.float64, device=acc.device)
-    _lib.check(lib.smm_finalize(_lib.VARIANT[variant], ptr(acc), ptr(polys), d, log2b, stream_ptr(acc.device)))
+    with torch.cuda.device(acc.device):
+        _lib.check(lib.smm_finalize(_lib.VARIANT[variant], ptr(acc), ptr(polys), d, log2b, stream_ptr(acc.device)))
     return polys
+
+
+def pair_capacity(rows: int, n2: int) -> int:
+    """Heavy-hitter pair buffer written without knowing the count (1/8 of the grid,
+    at least 64K pairs); a larger count is re-emitted from the kept bitmask."""
+    return int(min(rows * n2, max(1 << 16, (rows * n2) // 8)))
+
+
+class PendingPairs:
+    """Heavy-hitter pairs of one extract call, written on the device up to a capacity;
+    ``resolve()`` reads the device count (the call's only host sync) and re-emits
+    the list from the call's bitmask in the rare case it overflowed."""
+
+    def __init__(self, count, buf, ws, n2, r0, r1, dev):
+        self.count, self.buf, self.ws, self.n2, self.r0, self.r1, self.dev = count, buf, ws, n2, r0, r1, dev
+
+    def resolve(self, cnt: int | None = None) -> torch.Tensor:
+        cnt = int(self.count.item()) if cnt is None else cnt
+        if cnt > self.buf.shape[0]:
+            lib = _lib.load()
+            self.buf = torch.empty((cnt, 2), dtype=torch.int64, device=self.dev)
+            with torch.cuda.device(self.dev):
+                _lib.check(lib.smm_hh_pairs(ptr(self.ws), self.n2, self.r0, self.r1, ptr(self.buf), cnt,
+                                            stream_ptr(self.dev)))
+        self.ws = None
+        return self.buf[:cnt]
 
 
 def extract(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: str, n1: int, n2: int,
             r0: int = 0, r1: int | None = None, want_est: bool = True, thr: float = 0.5, strict: bool = True,
-            want_pairs: bool = False, est_out: torch.Tensor | None = None):
-    """Rows [r0, r1) of the estimate grid and the heavy hitters |est| >(=) thr."""
+            want_pairs: bool = False, est_out: torch.Tensor | None = None, defer_pairs: bool = False):
+    """Rows [r0, r1) of the estimate grid and the heavy hitters |est| >(=) thr.
+
+    The pair list is written by the kernel that follows the extraction with no
+    host round trip in between (capacity ``pair_capacity``); the count is read
+    once at the end, or never with ``defer_pairs`` (then ``pairs`` is a
+    ``PendingPairs`` to resolve later)."""
     lib = _lib.load()
     dev = polys.device
     r1 = n1 if r1 is None else r1
     rows = r1 - r0
-    nbytes = ctypes.c_int64(0)
-    _lib.check(lib.smm_extract_workspace(d, n1, n2, r0, r1, ctypes.byref(nbytes)))
-    ws = workspace(nbytes.value, dev)
-    est = est_out
-    if want_est and est is None:
-        est = torch.empty((rows, n2), dtype=torch.float64, device=dev)
-    count = torch.zeros(1, dtype=torch.int64, device=dev)
-    words, wp = words_ptr(words)
-    v = _lib.VARIANT[variant]
-    ld = est.stride(0) if est is not None else n2
-    _lib.check(lib.smm_extract(v, ptr(polys), wp, d, log2b, n1, n2, r0, r1, ptr(est), ld, float(thr),
-                               1 if strict else 0, None, 0, ptr(count), ptr(ws), ws.numel(), stream_ptr(dev)))
+    with torch.cuda.device(dev):
+        nbytes = ctypes.c_int64(0)
+        _lib.check(lib.smm_extract_workspace(d, n1, n2, r0, r1, ctypes.byref(nbytes)))
+        ws = workspace(nbytes.value, dev)
+        est = est_out
+        if want_est and est is None:
+            est = torch.empty((rows, n2), dtype=torch.float64, device=dev)
+        count = torch.zeros(1, dtype=torch.int64, device=dev)
+        words, wp = words_ptr(words)
+        v = _lib.VARIANT[variant]
+        ld = est.stride(0) if est is not None else n2
+        cap = pair_capacity(rows, n2) if want_pairs else 0
+        buf = torch.empty((cap, 2), dtype=torch.int64, device=dev) if want_pairs else None
+        _lib.check(lib.smm_extract(v, ptr(polys), wp, d, log2b, n1, n2, r0, r1, ptr(est), ld, float(thr),
+                                   1 if strict else 0, ptr(buf), cap, ptr(count), ptr(ws), ws.numel(),
+                                   stream_ptr(dev)))
     pairs = None
     if want_pairs:
-        cnt = int(count.item())
-        pairs = torch.empty((cnt, 2), dtype=torch.int64, device=dev)
-        if cnt:
-            # the bitmask of this extract call is still in `ws`: emit pairs without recomputing medians
-            _lib.check(lib.smm_hh_pairs(ptr(ws), n2, r0, r1, ptr(pairs), cnt, stream_ptr(dev)))
+        pairs = PendingPairs(count, buf, ws, n2, r0, r1, dev)
+        if not defer_pairs:
+            pairs = pairs.resolve()
     return est, count, pairs
 
 
@@ -296,8 +346,9 @@ def query(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, variant: s
     est = torch.empty(count, dtype=torch.float64, device=dev)
     reps = torch.empty((count, d), dtype=torch.float64, device=dev) if want_reps else None
     words, wp = words_ptr(words)
-    _lib.check(lib.smm_query(_lib.VARIANT[variant], ptr(polys), wp, d, log2b, n1, n2, ptr(ij), count, ptr(est),
-                             ptr(reps), stream_ptr(dev)))
+    with torch.cuda.device(dev):
+        _lib.check(lib.smm_query(_lib.VARIANT[variant], ptr(polys), wp, d, log2b, n1, n2, ptr(ij), count, ptr(est),
+                                 ptr(reps), stream_ptr(dev)))
     return est, reps
 
 
@@ -320,25 +371,30 @@ def extract_host(polys: torch.Tensor, words: np.ndarray, d: int, log2b: int, var
     ring = [torch.empty((R, n2), dtype=torch.float64, device=dev) for _ in range(min(2, -(-rows // R)))]
     ready = [torch.cuda.Event() for _ in ring]
     done = [torch.cuda.Event() for _ in ring]
-    pairs = []
-    for bi, q0 in enumerate(range(r0, r1, R)):
-        q1 = min(r1, q0 + R)
-        slot = bi % len(ring)
-        if bi >= len(ring):
-            compute.wait_event(done[slot])
-        _, _, pr = extract(polys, words, d, log2b, variant, n1, n2, q0, q1, want_est=True, thr=thr, strict=strict,
-                           want_pairs=True, est_out=ring[slot][:q1 - q0])
-        pairs.append(pr)
-        ready[slot].record(compute)
-        with torch.cuda.stream(copy):
-            copy.wait_event(ready[slot])
-            copy2d(est_host[q0 - r0:q1 - r0], ring[slot][:q1 - q0], copy)
-            done[slot].record(copy)
-    pairs = torch.cat(pairs) if len(pairs) > 1 else pairs[0]
-    pairs_host = torch.empty(pairs.shape, dtype=pairs.dtype, pin_memory=True)
-    pairs_host.copy_(pairs, non_blocking=True)  # on the compute stream, behind the last extraction
-    compute.wait_stream(copy)
-    compute.synchronize()
+    pending = []
+    with torch.cuda.device(dev):
+        copy.wait_stream(compute)  # ring blocks may reuse memory still in use on the compute stream
+        for bi, q0 in enumerate(range(r0, r1, R)):
+            q1 = min(r1, q0 + R)
+            slot = bi % len(ring)
+            if bi >= len(ring):
+                compute.wait_event(done[slot])
+            _, _, pr = extract(polys, words, d, log2b, variant, n1, n2, q0, q1, want_est=True, thr=thr,
+                               strict=strict, want_pairs=True, est_out=ring[slot][:q1 - q0], defer_pairs=True)
+            pending.append(pr)
+            ready[slot].record(compute)
+            with torch.cuda.stream(copy):
+                copy.wait_event(ready[slot])
+                copy2d(est_host[q0 - r0:q1 - r0], ring[slot][:q1 - q0], copy)
+                done[slot].record(copy)
+        # no host round trip per block: every block's count is read once, after all are queued
+        counts = torch.cat([pr.count for pr in pending]).cpu().tolist()
+        pairs = [pr.resolve(c) for pr, c in zip(pending, counts)]
+        pairs = torch.cat(pairs) if len(pairs) > 1 else pairs[0]
+        pairs_host = torch.empty(pairs.shape, dtype=pairs.dtype, pin_memory=True)
+        pairs_host.copy_(pairs, non_blocking=True)  # on the compute stream, behind the last extraction
+        compute.wait_stream(copy)
+        compute.synchronize()  # the reference's decompress_all is synchronous: est_host is complete
     return pairs_host
 
 
@@ -347,7 +403,8 @@ def fwht_batched(x: torch.Tensor, scale: float = 1.0) -> torch.Tensor:
     n = x.shape[-1]
     log2n = n.bit_length() - 1
     batch = x.numel() // n if n else 0
-    _lib.check(lib.smm_fwht_batched(ptr(x), batch, log2n, float(scale), stream_ptr(x.device)))
+    with torch.cuda.device(x.device):
+        _lib.check(lib.smm_fwht_batched(ptr(x), batch, log2n, float(scale), stream_ptr(x.device)))
     return x
 
 
@@ -357,5 +414,7 @@ def fft_batched(z: torch.Tensor, inverse: bool = False, scale: float = 1.0) -> t
     n = z.shape[-1]
     log2n = n.bit_length() - 1
     batch = z.numel() // n if n else 0
-    _lib.check(lib.smm_fft_batched(ptr(z), batch, log2n, 1 if inverse else 0, float(scale), stream_ptr(z.device)))
+    with torch.cuda.device(z.device):
+        _lib.check(lib.smm_fft_batched(ptr(z), batch, log2n, 1 if inverse else 0, float(scale),
+                                       stream_ptr(z.device)))
     return z

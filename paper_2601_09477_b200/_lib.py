@@ -22,7 +22,8 @@ SMM_ERR_INVALID = 1
 SMM_ERR_CUDA = 2
 SMM_ERR_WORKSPACE = 3
 VARIANT = {"fft": 0, "fwht": 1}
-MAX_DEPTH = 63
+MAX_DEPTH = 63  # repetitions per kernel launch (SMM_MAX_DEPTH)
+MAX_DEPTH_TOTAL = 511  # deepest sketch the device path handles (SMM_MAX_DEPTH_TOTAL)
 FLAG_ACCUMULATE = 0x100
 
 EXPORTS = (

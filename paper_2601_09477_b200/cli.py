@@ -1,11 +1,15 @@
 """Command line: the reference's ``multiply`` workflow on the B200 path.
 
     python -m paper_2601_09477_b200 [--seed S] [--threads T] [--transform fwht|fft] \\
+        [--format csv|json] [--max-mem BYTES] \\
         multiply A B -o OUT (--cd CD --cb CB | -b WIDTH -d DEPTH) [--save-sketch SKETCH]
 
-Same options, validation and exit codes as the reference (cli.py:133-199): 0 on
-success, 1 on runtime failures (I/O, formats, no GPU), 2 on usage or parameter
-errors.  The estimate matrix and the ``.skch`` container are written in the
+Same global options, validation and exit codes as the reference (cli.py:133-199):
+0 on success, 1 on runtime failures (I/O, formats, memory budget, no GPU), 2 on
+usage or parameter errors.  ``--max-mem`` applies the reference's budget check
+(cli.py:85-92: 1.25 x estimate_workspace_bytes against the budget) before any
+work; ``--format`` only selects the result-table format of the reference's
+experiment subcommands and is accepted for compatibility.  The estimate matrix and the ``.skch`` container are written in the
 reference's formats.  The reference's generator / experiment subcommands are
 outside this path.
 """
@@ -13,14 +17,34 @@ outside this path.
 from __future__ import annotations
 
 import functools
+import re
 import time
 
 import click
 
 from . import __version__
-from .errors import InvalidParameterError, SketchmmError
+from .errors import InvalidParameterError, MemoryBudgetError, SketchmmError
 from .matio import load_matrix, save_matrix
-from .sketch import SketchParams, compress, decompress_all, derive_params, effective_threads, save_sketch
+from .sketch import (SketchParams, compress, decompress_all, derive_params, effective_threads,
+                     estimate_workspace_bytes, save_sketch)
+
+
+def _parse_bytes(text: str) -> int:
+    """Memory size with an optional K/M/G/T suffix (cli.py:62-67)."""
+    m = re.fullmatch(r"\s*(\d+(?:\.\d+)?)\s*([kmgt]?)b?\s*", text, re.IGNORECASE)
+    if not m:
+        raise click.BadParameter(f"cannot parse memory size {text!r}")
+    scale = {"": 1, "k": 1 << 10, "m": 1 << 20, "g": 1 << 30, "t": 1 << 40}
+    return int(float(m.group(1)) * scale[m.group(2).lower()])
+
+
+def _check_budget(cfg: dict, n: int, b: int, d: int, transform: str) -> None:
+    """The reference's working-set check (cli.py:85-92), same estimate and margin."""
+    if cfg["max_mem"] is None:
+        return
+    need = int(1.25 * estimate_workspace_bytes(n, b, d, transform, effective_threads(cfg["threads"])))
+    if need > cfg["max_mem"]:
+        raise MemoryBudgetError(f"estimated working set {need} bytes exceeds --max-mem {cfg['max_mem']}")
 
 
 def _cli_errors(fn):
@@ -46,10 +70,15 @@ def _cli_errors(fn):
               help="Accepted for compatibility (device reduction order is fixed).")
 @click.option("--transform", type=click.Choice(["fft", "fwht"]), default="fwht", show_default=True,
               help="Sketch convolution variant.")
+@click.option("--format", "fmt", type=click.Choice(["csv", "json"]), default="csv", show_default=True,
+              help="Result table format of the reference's experiment subcommands (compatibility).")
+@click.option("--max-mem", type=str, default=None, metavar="BYTES",
+              help="Refuse runs whose estimated working set exceeds this budget (accepts K/M/G/T suffixes).")
 @click.pass_context
-def main(ctx, seed, threads, transform):
+def main(ctx, seed, threads, transform, fmt, max_mem):
     """Sketched matrix products on B200: estimate entries of A @ B from a small sketch."""
-    ctx.obj = {"seed": seed, "threads": threads, "transform": transform}
+    budget = _parse_bytes(max_mem) if max_mem is not None else None
+    ctx.obj = {"seed": seed, "threads": threads, "transform": transform, "fmt": fmt, "max_mem": budget}
 
 
 @main.command()
@@ -81,6 +110,7 @@ def multiply(cfg, a_file, b_file, out, cd, cb, buckets, depth, sketch_out):
         params = derive_params(n, cd, cb, transform=cfg["transform"], seed=cfg["seed"])
     else:
         params = SketchParams(n=n, b=buckets, d=depth, transform=cfg["transform"], seed=cfg["seed"])
+    _check_budget(cfg, n, params.b, params.d, params.transform)
     threads = effective_threads(cfg["threads"])
     t0 = time.perf_counter()
     sk = compress(a, b, params, threads=threads)

@@ -34,6 +34,12 @@ int hh_pairs(const void *ws, int64_t n2, int64_t r0, int64_t r1, int64_t *pairs,
 int query(int variant, const SketchHashes &h, const double *polys, const int64_t *ij, int64_t count, double *est,
           double *reps, cudaStream_t s);
 int64_t launches();
+int64_t big_hash_bytes(int d);
+int extract_big(int variant, const uint64_t *words, int d, int log2b, const double *polys, int64_t n2, int64_t r0,
+                int64_t r1, double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
+                int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s);
+int query_big(int variant, const uint64_t *words, int d, int log2b, const double *polys, const int64_t *ij,
+              int64_t count, double *est, double *reps, cudaStream_t s);
 int transpose(const double *in, int64_t rows, int64_t cols, int64_t ld_in, double *out, int64_t ld_out,
               cudaStream_t s);
 int fwht_batched(double *x, int64_t batch, int log2n, double scale, cudaStream_t s);
@@ -60,11 +66,22 @@ static int64_t acc_bytes(int variant, int d, int log2b) {
 // extraction needs an odd d (the median is the middle order statistic).
 static int check_sketch(int variant, int d, int log2b, bool need_odd = false) {
   SMM_REQUIRE(variant == SMM_VARIANT_FFT || variant == SMM_VARIANT_FWHT, "unknown transform variant %d", variant);
-  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH, "d must be in [1, %d], got %d", SMM_MAX_DEPTH, d);
-  SMM_REQUIRE(!need_odd || d % 2 == 1, "d must be an odd integer in [1, %d], got %d", SMM_MAX_DEPTH, d);
+  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH_TOTAL, "d must be in [1, %d], got %d", SMM_MAX_DEPTH_TOTAL, d);
+  SMM_REQUIRE(!need_odd || d % 2 == 1, "d must be an odd integer in [1, %d], got %d", SMM_MAX_DEPTH_TOTAL, d);
   SMM_REQUIRE(log2b >= 1 && log2b <= 32, "b must be a power of two in [2, 2**32], got 2**%d", log2b);
   if (variant == SMM_VARIANT_FFT) SMM_REQUIRE(log2b <= 30, "fft variant supports b <= 2**30");
   return SMM_OK;
+}
+
+// Hash words of repetitions [t0, t1) in the group-major layout of words_host
+// (hashing.py:146-152): the input of one kernel launch of at most SMM_MAX_DEPTH.
+static void group_words(const uint64_t *words, int d, int t0, int t1, uint64_t *out) {
+  const int dg = t1 - t0;
+  for (int g = 0; g < 4; ++g)
+    for (int t = 0; t < dg; ++t) {
+      out[g * 2 * dg + 2 * t] = words[g * 2 * d + 2 * (t0 + t)];
+      out[g * 2 * dg + 2 * t + 1] = words[g * 2 * d + 2 * (t0 + t) + 1];
+    }
 }
 
 extern "C" {
@@ -76,15 +93,23 @@ const char *smm_last_error(void) { return last_error(); }
 int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int64_t n, uint32_t *buckets_out,
                     int8_t *signs_out, void *stream) {
   SMM_REQUIRE(words_host != nullptr, "hash words must not be NULL");
-  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH, "d out of range");
+  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH_TOTAL, "d out of range");
   SMM_REQUIRE(log2b >= 1 && log2b <= 32, "log2b out of range");
   SMM_REQUIRE(group >= 0 && group <= 3, "group must be 0..3");
   SMM_REQUIRE(n >= 0 && n <= ((int64_t)1 << 32), "keys must fit in 32 bits");
   SMM_REQUIRE(group >= 2 || buckets_out != nullptr, "buckets_out is NULL");
   SMM_REQUIRE(group < 2 || signs_out != nullptr, "signs_out is NULL");
-  SketchHashes h;
-  load_hashes(h, words_host, d, log2b);
-  return hash_tables(h, group, n, buckets_out, signs_out, (cudaStream_t)stream);
+  uint64_t gw[8 * SMM_MAX_DEPTH];
+  for (int t0 = 0; t0 < d; t0 += SMM_MAX_DEPTH) {  // repetition groups of one launch each
+    const int t1 = t0 + SMM_MAX_DEPTH < d ? t0 + SMM_MAX_DEPTH : d;
+    group_words(words_host, d, t0, t1, gw);
+    SketchHashes h;
+    load_hashes(h, gw, t1 - t0, log2b);
+    const int rc = hash_tables(h, group, n, buckets_out ? buckets_out + (int64_t)t0 * n : nullptr,
+                               signs_out ? signs_out + (int64_t)t0 * n : nullptr, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return SMM_OK;
 }
 
 // ---------------------------------------------------------------- compress dispatch
@@ -128,7 +153,8 @@ int smm_compress_workspace_ex(int variant, int d, int log2b, int64_t n1, int64_t
   SMM_REQUIRE(bytes != nullptr, "bytes is NULL");
   SMM_REQUIRE(n1 >= 0 && n2 >= 0 && k0 >= 0 && k1 >= k0, "bad shapes");
   SMM_REQUIRE((a_layout == 0 || a_layout == 1) && (b_layout == 0 || b_layout == 1), "bad layout");
-  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, k1 - k0, a_layout, b_layout, acc_add);
+  const int dg = d < SMM_MAX_DEPTH ? d : SMM_MAX_DEPTH;  // one launch's repetitions (workspace reused per group)
+  CompressPlan c = plan_compress(variant, dg, log2b, n1, n2, k1 - k0, a_layout, b_layout, acc_add);
   *bytes = c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes + c.kernel_bytes;
   return SMM_OK;
 }
@@ -153,11 +179,10 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
   SMM_REQUIRE(k1 == k0 || ((a != nullptr || n1 == 0) && (b != nullptr || n2 == 0)), "operand pointer is NULL");
   SMM_REQUIRE(a_layout == SMM_LAYOUT_KMAJOR ? lda >= n1 : lda >= k1, "lda too small for the layout");
   SMM_REQUIRE(b_layout == SMM_LAYOUT_KMAJOR ? ldb >= n2 : ldb >= k1, "ldb too small for the layout");
-  SketchHashes h;
-  load_hashes(h, words_host, d, log2b);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t K = k1 - k0;
-  CompressPlan c = plan_compress(variant, d, log2b, n1, n2, K, a_layout, b_layout, acc_add);
+  const int dg = d < SMM_MAX_DEPTH ? d : SMM_MAX_DEPTH;
+  CompressPlan c = plan_compress(variant, dg, log2b, n1, n2, K, a_layout, b_layout, acc_add);
   const int64_t need = c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes + c.kernel_bytes;
   if (workspace_bytes < need) {
     set_error("compress workspace too small: %lld < %lld bytes", (long long)workspace_bytes, (long long)need);
@@ -194,16 +219,29 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
   }
   char *kws = ws + c.ta_bytes + c.tb_bytes + c.tmp_acc_bytes;
   const int64_t kb = workspace_bytes - c.ta_bytes - c.tb_bytes - c.tmp_acc_bytes;
-  if (c.fft_two_pass)
-    return fft2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, acc_add, kws, kb, s);
-  if (c.two_pass) return fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)acc, acc_add, kws, kb, s);
-  void *dst = acc_add ? (void *)(ws + c.ta_bytes + c.tb_bytes) : acc;
-  if (variant == SMM_VARIANT_FWHT)
-    rc = fwht_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)dst, kws, kb, s);
-  else
-    rc = fft_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (cplx *)dst, kws, kb, s);
-  if (rc || !acc_add) return rc;
-  return add_inplace((double *)acc, (const double *)dst, acc_bytes(variant, d, log2b) / 8, s);
+  // repetition groups of at most SMM_MAX_DEPTH, one launch each, into rows [t0, t1) of acc
+  uint64_t gw[8 * SMM_MAX_DEPTH];
+  for (int t0 = 0; t0 < d; t0 += SMM_MAX_DEPTH) {
+    const int t1 = t0 + SMM_MAX_DEPTH < d ? t0 + SMM_MAX_DEPTH : d;
+    group_words(words_host, d, t0, t1, gw);
+    SketchHashes h;
+    load_hashes(h, gw, t1 - t0, log2b);
+    char *accg = (char *)acc + acc_bytes(variant, t0, log2b);
+    if (c.fft_two_pass)
+      rc = fft2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)accg, acc_add, kws, kb, s);
+    else if (c.two_pass)
+      rc = fwht2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)accg, acc_add, kws, kb, s);
+    else {
+      void *dst = acc_add ? (void *)(ws + c.ta_bytes + c.tb_bytes) : (void *)accg;
+      if (variant == SMM_VARIANT_FWHT)
+        rc = fwht_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)dst, kws, kb, s);
+      else
+        rc = fft_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (cplx *)dst, kws, kb, s);
+      if (!rc && acc_add) rc = add_inplace((double *)accg, (const double *)dst, acc_bytes(variant, t1 - t0, log2b) / 8, s);
+    }
+    if (rc) return rc;
+  }
+  return SMM_OK;
 }
 
 int smm_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t rows,
@@ -232,11 +270,11 @@ int smm_finalize(int variant, const void *acc, double *polys, int d, int log2b, 
 }
 
 int smm_extract_workspace(int d, int64_t n1, int64_t n2, int64_t r0, int64_t r1, int64_t *bytes) {
-  (void)d;
   SMM_REQUIRE(bytes != nullptr, "bytes is NULL");
+  SMM_REQUIRE(d >= 1 && d <= SMM_MAX_DEPTH_TOTAL, "d must be in [1, %d], got %d", SMM_MAX_DEPTH_TOTAL, d);
   SMM_REQUIRE(r0 >= 0 && r1 >= r0 && r1 <= n1 && n2 >= 0, "row range [%lld, %lld) outside %lld rows", (long long)r0,
               (long long)r1, (long long)n1);
-  *bytes = extract_workspace(n2, r0, r1);
+  *bytes = extract_workspace(n2, r0, r1) + big_hash_bytes(d);
   return SMM_OK;
 }
 
@@ -252,6 +290,9 @@ int smm_extract(int variant, const double *polys, const uint64_t *words_host, in
   SMM_REQUIRE(n1 <= ((int64_t)1 << 32) && n2 <= ((int64_t)1 << 32), "keys must fit in 32 bits");
   SMM_REQUIRE(est == nullptr || ld_est >= n2, "ld_est < n2");
   SMM_REQUIRE(hh_cap >= 0, "hh_cap < 0");
+  if (d > SMM_MAX_DEPTH)
+    return extract_big(variant, words_host, d, log2b, polys, n2, r0, r1, est, ld_est, thr, strict, hh_pairs, hh_cap,
+                       hh_count, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
   SketchHashes h;
   load_hashes(h, words_host, d, log2b);
   return extract(variant, h, polys, n1, n2, r0, r1, est, ld_est, thr, strict, hh_pairs, hh_cap, hh_count,
@@ -274,6 +315,7 @@ int smm_query(int variant, const double *polys, const uint64_t *words_host, int 
   SMM_REQUIRE(count == 0 || (polys != nullptr && words_host != nullptr && ij != nullptr && est != nullptr),
               "NULL argument");
   SMM_REQUIRE(n1 <= ((int64_t)1 << 32) && n2 <= ((int64_t)1 << 32), "keys must fit in 32 bits");
+  if (d > SMM_MAX_DEPTH) return query_big(variant, words_host, d, log2b, polys, ij, count, est, reps, (cudaStream_t)stream);
   SketchHashes h;
   load_hashes(h, words_host, d, log2b);
   return query(variant, h, polys, ij, count, est, reps, (cudaStream_t)stream);

@@ -42,6 +42,8 @@ struct KernelTimer {
 int l2_policies(uint64_t &evict_last, uint64_t &evict_first);
 void kernel_timing(int on);
 int kernel_timing_read(int channel, double *total_ms, int64_t *count);
+// keep freed stream-ordered scratch in the device's default pool (transforms.cu)
+void keep_pool_memory();
 
 // ---------------------------------------------------------------- hashing
 // One drawn hash function (hashing.py:35-51): bucket = ((a*x + c) mod 2^64) >> shift.

@@ -229,6 +229,103 @@ __global__ void query_kernel(SketchHashes h, const double *polys, const int64_t 
   }
 }
 
+// ---------------------------------------------------------------- depth > SMM_MAX_DEPTH
+// The reference accepts any odd d (sketch.py:75-76).  Past the kernel-parameter
+// hash block (63 repetitions) the hash functions come from a device array
+// hf[4][d] and each thread keeps its d values in its own shared-memory column
+// (stride = threads per CTA: conflict-free), sorted in place by insertion sort —
+// the exact middle order statistic, NaN in -> NaN out, as np.median.
+template <bool XOR>
+__device__ __forceinline__ double big_entry(const HashFn *hf, int d, int log2b, const double *polys, uint64_t i,
+                                            uint64_t j, double *col, int stride, double *reps) {
+  const uint32_t bmask = (uint32_t)(((uint64_t)1 << log2b) - 1);
+  const int64_t b = (int64_t)1 << log2b;
+  bool has_nan = false;
+  for (int t = 0; t < d; ++t) {
+    const uint32_t a = eval_bucket(hf[t], i, log2b), c = eval_bucket(hf[d + t], j, log2b);
+    const uint32_t idx = XOR ? (a ^ c) : ((a + c) & bmask);
+    double x = __ldg(polys + t * b + idx);
+    x *= eval_signbit(hf[2 * d + t], i) ? -1.0 : 1.0;  // vals *= s1 ; vals *= s2 (sketch.py:396-397)
+    x *= eval_signbit(hf[3 * d + t], j) ? -1.0 : 1.0;
+    if (reps) reps[t] = x;
+    has_nan |= isnan(x);
+    int k = t - 1;  // insertion into the sorted prefix
+    while (k >= 0 && col[k * stride] > x) {
+      col[(k + 1) * stride] = col[k * stride];
+      --k;
+    }
+    col[(k + 1) * stride] = x;
+  }
+  return has_nan ? __longlong_as_double(0x7ff8000000000000ll) : col[((d - 1) / 2) * stride];
+}
+
+struct BigArgs {
+  const HashFn *hf;
+  int d, log2b, xor_combine;
+  const double *polys;
+  int64_t n2, r0, r1;
+  double *est;
+  int64_t ld_est;
+  double thr;
+  int strict;
+  uint32_t *mask;
+  int64_t mask_ld;
+  int64_t *rowcnt;
+};
+
+// grid (ceil(n2 / blockDim), rows): one row per CTA row, one column per thread
+__global__ void extract_big_kernel(BigArgs p) {
+  extern __shared__ double sv[];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = p.r0 + blockIdx.y;
+  const bool colok = j < p.n2;
+  double e = 0.0;
+  if (colok) {
+    e = p.xor_combine ? big_entry<true>(p.hf, p.d, p.log2b, p.polys, (uint64_t)i, (uint64_t)j, sv + threadIdx.x,
+                                        blockDim.x, nullptr)
+                      : big_entry<false>(p.hf, p.d, p.log2b, p.polys, (uint64_t)i, (uint64_t)j, sv + threadIdx.x,
+                                         blockDim.x, nullptr);
+    if (p.est) p.est[(i - p.r0) * p.ld_est + j] = e;
+  }
+  const double ae = fabs(e);
+  const bool hit = colok && (p.strict ? (ae > p.thr) : (ae >= p.thr));
+  const unsigned bal = __ballot_sync(0xffffffffu, hit);
+  if ((threadIdx.x & 31) == 0 && (j >> 5) < p.mask_ld) {
+    p.mask[(i - p.r0) * p.mask_ld + (j >> 5)] = bal;
+    if (bal) atomicAdd((unsigned long long *)&p.rowcnt[i - p.r0], (unsigned long long)__popc(bal));
+  }
+}
+
+__global__ void query_big_kernel(const HashFn *hf, int d, int log2b, const double *polys, const int64_t *ij,
+                                 int64_t count, int xor_combine, double *est, double *reps) {
+  extern __shared__ double sv[];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)ij[2 * q], j = (uint64_t)ij[2 * q + 1];
+    double *r = reps ? reps + q * d : nullptr;
+    est[q] = xor_combine ? big_entry<true>(hf, d, log2b, polys, i, j, sv + threadIdx.x, blockDim.x, r)
+                         : big_entry<false>(hf, d, log2b, polys, i, j, sv + threadIdx.x, blockDim.x, r);
+  }
+}
+
+// threads per CTA for the big-depth kernels: d doubles per thread in shared memory
+static int big_threads(int d) {
+  int th = 256;
+  while (th > 32 && (int64_t)th * d * 8 > 200 * 1024) th /= 2;
+  return th;
+}
+
+int64_t big_hash_bytes(int d) { return d > SMM_MAX_DEPTH ? (((int64_t)d * 4 * 16 + 255) / 256) * 256 : 0; }
+
+// upload hf[4][d] (group-major draw order, hashing.py:146-152) into dev
+static int upload_hashes(HashFn *dev, const uint64_t *words, int d, cudaStream_t s) {
+  SMM_CUDA_TRY(cudaMemcpyAsync(dev, words, (size_t)d * 4 * 16, cudaMemcpyHostToDevice, s), "hash upload");
+  return SMM_OK;
+}
+
+int extract_big(int variant, const uint64_t *words, int d, int log2b, const double *polys, int64_t n2, int64_t r0,
+                int64_t r1, double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
+                int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s);
+
 int query(int variant, const SketchHashes &h, const double *polys, const int64_t *ij, int64_t count, double *est,
           double *reps, cudaStream_t s) {
   if (count <= 0) return SMM_OK;
@@ -277,21 +374,109 @@ int extract(int variant, const SketchHashes &h, const double *polys, int64_t n1,
     return SMM_OK;
   }
   SMM_CUDA_TRY(cudaMemsetAsync(p.rowcnt, 0, rows * 8, s), "extract memset");
-  dim3 grid((unsigned)ceil_div(n2, XT), (unsigned)ceil_div(rows, XROWS));
   KernelTimer timer(1, s);
-  switch (h.d) {
-    case 1: extract_kernel<1><<<grid, XT, 0, s>>>(p); break;
-    case 3: extract_kernel<3><<<grid, XT, 0, s>>>(p); break;
-    case 5: extract_kernel<5><<<grid, XT, 0, s>>>(p); break;
-    case 7: extract_kernel<7><<<grid, XT, 0, s>>>(p); break;
-    case 9: extract_kernel<9><<<grid, XT, 0, s>>>(p); break;
-    default: extract_kernel<0><<<grid, XT, 0, s>>>(p); break;
+  const int64_t chunk = (int64_t)65535 * XROWS;  // grid.y limit: row chunks of 65535 tiles
+  for (int64_t y0 = 0; y0 < rows; y0 += chunk) {
+    ExtractArgs pc = p;
+    pc.r0 = r0 + y0;
+    pc.r1 = y0 + chunk < rows ? r0 + y0 + chunk : r1;
+    pc.est = est ? est + y0 * ld_est : nullptr;
+    pc.mask = p.mask + y0 * p.mask_ld;
+    pc.rowcnt = p.rowcnt + y0;
+    dim3 grid((unsigned)ceil_div(n2, XT), (unsigned)ceil_div(pc.r1 - pc.r0, XROWS));
+    switch (h.d) {
+      case 1: extract_kernel<1><<<grid, XT, 0, s>>>(pc); break;
+      case 3: extract_kernel<3><<<grid, XT, 0, s>>>(pc); break;
+      case 5: extract_kernel<5><<<grid, XT, 0, s>>>(pc); break;
+      case 7: extract_kernel<7><<<grid, XT, 0, s>>>(pc); break;
+      case 9: extract_kernel<9><<<grid, XT, 0, s>>>(pc); break;
+      default: extract_kernel<0><<<grid, XT, 0, s>>>(pc); break;
+    }
   }
   timer.stop();
   SMM_LAUNCH_CHECK("extract_kernel");
   row_scan_kernel<<<1, 1024, 0, s>>>(p.rowcnt, rows, offs, hh_count);
   SMM_LAUNCH_CHECK("row_scan_kernel");
   if (hh_pairs && hh_cap > 0) return smm::hh_pairs(ws, n2, r0, r1, hh_pairs, hh_cap, s);
+  return SMM_OK;
+}
+
+
+int extract_big(int variant, const uint64_t *words, int d, int log2b, const double *polys, int64_t n2, int64_t r0,
+                int64_t r1, double *est, int64_t ld_est, double thr, int strict, int64_t *hh_pairs, int64_t hh_cap,
+                int64_t *hh_count, char *ws, int64_t ws_bytes, cudaStream_t s) {
+  const int64_t rows = r1 - r0;
+  const int64_t base = extract_workspace(n2, r0, r1);
+  if (ws_bytes < base + big_hash_bytes(d)) {
+    set_error("extract workspace too small");
+    return SMM_ERR_WORKSPACE;
+  }
+  BigArgs p;
+  p.hf = (const HashFn *)(ws + base);
+  p.d = d;
+  p.log2b = log2b;
+  p.xor_combine = variant == SMM_VARIANT_FWHT ? 1 : 0;
+  p.polys = polys;
+  p.n2 = n2;
+  p.r0 = r0;
+  p.r1 = r1;
+  p.est = est;
+  p.ld_est = ld_est;
+  p.thr = thr;
+  p.strict = strict;
+  p.mask_ld = ceil_div(n2, 32);
+  p.mask = (uint32_t *)ws;
+  char *q = ws + ((rows * p.mask_ld * 4 + 255) / 256) * 256;
+  p.rowcnt = (int64_t *)q;
+  int64_t *offs = (int64_t *)(q + ((rows * 8 + 255) / 256) * 256);
+  if (rows <= 0 || n2 <= 0) {
+    SMM_CUDA_TRY(cudaMemsetAsync(hh_count, 0, sizeof(int64_t), s), "extract memset");
+    return SMM_OK;
+  }
+  int rc = upload_hashes((HashFn *)p.hf, words, d, s);
+  if (rc) return rc;
+  SMM_CUDA_TRY(cudaMemsetAsync(p.rowcnt, 0, rows * 8, s), "extract memset");
+  const int th = big_threads(d);
+  const size_t smem = (size_t)th * d * 8;
+  SMM_CUDA_TRY(cudaFuncSetAttribute(extract_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "extract_big smem");
+  KernelTimer timer(1, s);
+  for (int64_t y0 = 0; y0 < rows; y0 += 65535) {  // grid.y limit
+    BigArgs pc = p;
+    pc.r0 = r0 + y0;
+    pc.r1 = y0 + 65535 < rows ? r0 + y0 + 65535 : r1;
+    pc.est = est ? est + y0 * ld_est : nullptr;
+    pc.mask = p.mask + y0 * p.mask_ld;
+    pc.rowcnt = p.rowcnt + y0;
+    dim3 grid((unsigned)ceil_div(n2, th), (unsigned)(pc.r1 - pc.r0));
+    extract_big_kernel<<<grid, th, smem, s>>>(pc);
+  }
+  timer.stop();
+  SMM_LAUNCH_CHECK("extract_big_kernel");
+  row_scan_kernel<<<1, 1024, 0, s>>>(p.rowcnt, rows, offs, hh_count);
+  SMM_LAUNCH_CHECK("row_scan_kernel");
+  if (hh_pairs && hh_cap > 0) return smm::hh_pairs(ws, n2, r0, r1, hh_pairs, hh_cap, s);
+  return SMM_OK;
+}
+
+int query_big(int variant, const uint64_t *words, int d, int log2b, const double *polys, const int64_t *ij,
+              int64_t count, double *est, double *reps, cudaStream_t s) {
+  if (count <= 0) return SMM_OK;
+  HashFn *hf = nullptr;
+  keep_pool_memory();
+  SMM_CUDA_TRY(cudaMallocAsync((void **)&hf, (size_t)d * 4 * 16, s), "query alloc");
+  int rc = upload_hashes(hf, words, d, s);
+  if (rc) return rc;
+  const int th = big_threads(d);
+  const size_t smem = (size_t)th * d * 8;
+  SMM_CUDA_TRY(cudaFuncSetAttribute(query_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "query_big smem");
+  int64_t blocks = ceil_div(count, th);
+  if (blocks > 4096) blocks = 4096;
+  query_big_kernel<<<(unsigned)blocks, th, smem, s>>>(hf, d, log2b, polys, ij, count,
+                                                      variant == SMM_VARIANT_FWHT ? 1 : 0, est, reps);
+  SMM_LAUNCH_CHECK("query_big_kernel");
+  SMM_CUDA_TRY(cudaFreeAsync(hf, s), "query free");
   return SMM_OK;
 }
 

@@ -118,7 +118,7 @@ __global__ void cscale_kernel(cplx *z, int64_t n, double scale) {
 // with its default release threshold (0) every synchronisation returns the memory
 // to the driver and the next cudaMallocAsync maps it again (milliseconds of host
 // time while the GPU idles).  Keep freed blocks in the pool.
-static void keep_pool_memory() {
+void keep_pool_memory() {
   static std::atomic<bool> done[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || done[dev].load(std::memory_order_relaxed)) return;

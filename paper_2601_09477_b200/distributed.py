@@ -22,16 +22,30 @@ from .hashing import SketchHashes
 from .sketch import ProductSketch, SketchParams, effective_threads
 
 
-def shard_bounds(m: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous, balanced split of range(m) (same rule as sketch.py:117-120)."""
-    if world < 1 or not (0 <= rank < world):
-        raise InvalidParameterError(f"bad rank {rank} for world size {world}")
+K_TILE = 32  # inner indices per k-tile of the compress kernels
+
+
+def _balanced(m: int, world: int, rank: int) -> tuple[int, int]:
     edges = np.linspace(0, m, world + 1).astype(np.int64)
     return int(edges[rank]), int(edges[rank + 1])
 
 
+def shard_bounds(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous k-slab of rank ``rank``: whole 32-index k-tiles split as evenly as
+    possible (slabs then start on tile boundaries and keep the 16-byte pair mapping
+    of the compress kernels; the last rank also takes the partial tail tile)."""
+    if world < 1 or not (0 <= rank < world):
+        raise InvalidParameterError(f"bad rank {rank} for world size {world}")
+    tiles = -(-m // K_TILE)
+    t0, t1 = _balanced(tiles, world, rank)
+    return min(m, t0 * K_TILE), min(m, t1 * K_TILE)
+
+
 def row_bounds(n_rows: int, world: int, rank: int) -> tuple[int, int]:
-    return shard_bounds(n_rows, world, rank)
+    """Contiguous, balanced block of output rows (step 5 is row-sharded)."""
+    if world < 1 or not (0 <= rank < world):
+        raise InvalidParameterError(f"bad rank {rank} for world size {world}")
+    return _balanced(n_rows, world, rank)
 
 
 def compress_sharded(a_slab, b_slab, params: SketchParams, n_rows: int | None = None, n_cols: int | None = None,

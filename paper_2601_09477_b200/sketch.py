@@ -253,10 +253,13 @@ def _dispatch(a, b, params, threads, a_layout, dev, what_a):
 
 
 def _check_depth(params: SketchParams) -> None:
-    from ._lib import MAX_DEPTH
+    # any odd d as the reference (sketch.py:75-76), up to the device path's limit; past
+    # 63 repetitions the kernels run in groups of 63 and extraction reads the hashes
+    # from device memory
+    from ._lib import MAX_DEPTH_TOTAL
 
-    if params.d > MAX_DEPTH:
-        raise InvalidParameterError(f"d={params.d} exceeds the device kernels' maximum depth {MAX_DEPTH}")
+    if params.d > MAX_DEPTH_TOTAL:
+        raise InvalidParameterError(f"d={params.d} exceeds the device path's maximum depth {MAX_DEPTH_TOTAL}")
 
 
 def compress(a, b, params: SketchParams, threads: int | None = None, device=None) -> ProductSketch:

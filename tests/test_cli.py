@@ -68,3 +68,22 @@ def test_cli_multiply_writes_estimates_and_sketch(tmp_path):
         sk = P.compress(a, b, p)
         assert np.array_equal(matio.load_matrix(out), P.decompress_all(sk))
         assert P.load_sketch(skp) == sk
+
+
+def test_cli_global_options_max_mem_and_format(tmp_path):
+    """--max-mem applies the reference's budget check (cli.py:85-92) before any device
+    work: an over-budget run exits 1; --format is accepted (reference global option)."""
+    a = tmp_path / "a.dmat"
+    matio.save_matrix(a, np.eye(64))
+    args = ["multiply", str(a), str(a), "-o", str(tmp_path / "o.dmat"), "-b", "4096", "-d", "5"]
+    r = CliRunner().invoke(main, ["--max-mem", "1K"] + args)
+    assert r.exit_code == 1 and "exceeds --max-mem" in r.output
+    r = CliRunner().invoke(main, ["--max-mem", "lots"] + args)
+    assert r.exit_code == 2
+    need = int(1.25 * P.estimate_workspace_bytes(64, 4096, 5, "fwht", 1))
+    assert need > 1024
+    r = CliRunner().invoke(main, ["--format", "xml"] + args)
+    assert r.exit_code == 2
+    from paper_2601_09477_b200.cli import _parse_bytes
+
+    assert _parse_bytes("4G") == 4 << 30 and _parse_bytes("1.5k") == 1536 and _parse_bytes("10") == 10

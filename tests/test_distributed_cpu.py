@@ -64,12 +64,18 @@ def _worker(rank, world, port, q):
 
 
 def test_shard_bounds_partition():
-    for m in (0, 1, 7, 1000):
-        for world in (1, 2, 3, 8):
+    for m in (0, 1, 7, 1000, 16384, 16400, 32768 + 5):
+        for world in (1, 2, 3, 5, 8):
             parts = [D.shard_bounds(m, world, r) for r in range(world)]
             assert parts[0][0] == 0 and parts[-1][1] == m
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
-            assert max(p[1] - p[0] for p in parts) - min(p[1] - p[0] for p in parts) <= 1
+            # every slab starts on a 32-index k-tile boundary; whole tiles split evenly
+            assert all(p[0] % 32 == 0 for p in parts)
+            tiles = [-(-(p[1] - p[0]) // 32) for p in parts]
+            assert max(tiles) - min(tiles) <= 1
+            rows = [D.row_bounds(m, world, r) for r in range(world)]
+            assert rows[0][0] == 0 and rows[-1][1] == m
+            assert max(r[1] - r[0] for r in rows) - min(r[1] - r[0] for r in rows) <= 1
     plan = D.plan_shards(16384, 16384, 8)
     assert [p["k1"] - p["k0"] for p in plan] == [2048] * 8
 

@@ -77,15 +77,16 @@ def test_hash_tables_match_oracle_on_config_sizes():
         assert np.array_equal(_device.hash_table(h, 3, n).cpu().numpy().astype(np.float64), s2)
 
 
-# every BASELINE point with a reference golden (tools/make_golden.py): cfg1-3 and the cfg5 sweep
-CONFIGS = ["cfg1", "cfg2", "cfg3"] + sorted(p.stem for p in (Path(__file__).parent / "golden").glob("cfg5_*.npz"))
+# every BASELINE point (cfg1-3 and all 90 points of the cfg5 sweep) against its reference
+# golden (tools/make_golden.py); a missing golden is a failure, not a skip
+CONFIGS = ["cfg1", "cfg2", "cfg3"] + [W.cfg5_name(b, d, nnz, tr) for b in W.CFG5_B for d in W.CFG5_D
+                                      for nnz in W.CFG5_NNZ for tr in ("fwht", "fft")]
 
 
 @pytest.mark.parametrize("name", CONFIGS)
 def test_config_matches_reference(name):
     g = cfg_golden(name)
-    if g is None:
-        pytest.skip(f"no golden for {name}")
+    assert g is not None, f"no reference golden for BASELINE point {name} (tools/make_golden.py)"
     w = W.make(name, xp=torch, device="cuda")
     p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
     sk = P.compress(w.a, w.bmat, p)
@@ -105,10 +106,13 @@ def test_config_matches_reference(name):
     ij = torch.as_tensor(g["est_sample_ij"], device="cuda")
     e = est[ij[:, 0], ij[:, 1]].cpu().numpy()
     assert np.max(np.abs(e - g["est_sample"])) <= TOL * cn
+    # row sums of the full estimate grid (each estimate within TOL * cn, n2 per row)
+    assert np.max(np.abs(est.sum(dim=1).cpu().numpy() - g["est_rowsum"])) <= TOL * cn * w.n
     big = torch.as_tensor(w.big, device="cuda")
     if big.numel():
         eb = est[big[:, 0], big[:, 1]].cpu().numpy()
         assert np.max(np.abs(eb - g["est_big"])) <= TOL * cn
+    del est
     hh = P.heavy_hitters(sk, w.threshold, strict=True)
     assert hh.shape[0] == int(g["hh_count"][0])
     assert _sha(hh.astype(np.int64)) == bytes(g["hh_sha256"]).decode()
@@ -160,12 +164,19 @@ def test_cfg4_full_size_properties():
     big = torch.as_tensor(w.big, device="cuda")
     assert float((est[big[:, 0], big[:, 1]].abs() > 0.5).float().mean()) > 0.95
     g = cfg_golden("cfg4")
-    if g is not None:
-        samp = np.take_along_axis(sk.polys, g["polys_sample_idx"], axis=1)
-        assert np.max(np.abs(samp - g["polys_sample"])) <= TOL * cn
-        hh = P.heavy_hitters(sk, w.threshold, strict=True)
-        assert hh.shape[0] == int(g["hh_count"][0])
-        assert _sha(hh.astype(np.int64)) == bytes(g["hh_sha256"]).decode()
+    assert g is not None, "no reference golden for cfg4"
+    samp = np.take_along_axis(sk.polys, g["polys_sample_idx"], axis=1)
+    assert np.max(np.abs(samp - g["polys_sample"])) <= TOL * cn
+    assert np.allclose(sk.polys.sum(axis=1), g["polys_rowsum"], rtol=0, atol=TOL * cn * w.b)
+    # estimates: the golden's 4096 sampled entries and every row sum of the n x n grid
+    ij = torch.as_tensor(g["est_sample_ij"], device="cuda")
+    assert np.max(np.abs(est[ij[:, 0], ij[:, 1]].cpu().numpy() - g["est_sample"])) <= TOL * cn
+    assert np.max(np.abs(est.sum(dim=1).cpu().numpy() - g["est_rowsum"])) <= TOL * cn * w.n
+    assert np.max(np.abs(est[big[:, 0], big[:, 1]].cpu().numpy() - g["est_big"])) <= TOL * cn
+    del est
+    hh = P.heavy_hitters(sk, w.threshold, strict=True)
+    assert hh.shape[0] == int(g["hh_count"][0])
+    assert _sha(hh.astype(np.int64)) == bytes(g["hh_sha256"]).decode()
 
 
 def test_determinism_and_threads_independence():
@@ -508,3 +519,56 @@ def test_accumulator_slow_path_bit_identical(tmp_path):
     # one call and two accumulate-mode calls agree as well (FWHT two-pass: bit for bit)
     for i in (0, 2, 4):
         assert np.array_equal(res["fast"][i], res["fast"][i + 1]), i
+
+
+
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+def test_compress_seeds_stacked_against_oracle(transform):
+    """Three seeds stacked into one launch (compress_seeds) against the CPU oracle of
+    each seed separately (the reference's Monte-Carlo drivers call compress once per
+    seed, experiments.py:216-312)."""
+    rng = np.random.default_rng(41)
+    n = 384
+    a, m = rng.normal(size=(n, n)), rng.normal(size=(n, n))
+    p = P.SketchParams(n=n, b=1 << 12, d=5, transform=transform, seed=1)
+    seeds = [101, 202, 303]
+    sks = P.compress_seeds(a, m, p, seeds)
+    cn = _cnorm(a, m)
+    for sk, seed in zip(sks, seeds):
+        ref = O.compress(a, m, b=p.b, d=p.d, transform=transform, seed=seed, threads=8)
+        assert sk.params.seed == seed
+        assert np.max(np.abs(sk.polys - ref)) <= TOL * cn
+        eref, _, _ = O.decompress(ref, O.draw_words(seed, p.d, p.b), b=p.b, d=p.d, transform=transform, n1=n, n2=n)
+        assert np.max(np.abs(P.decompress_all(sk) - eref)) <= TOL * cn
+
+
+@pytest.mark.parametrize("transform,d,b", [("fwht", 65, 1 << 10), ("fft", 65, 1 << 9), ("fwht", 129, 1 << 12),
+                                           ("fft", 101, 1 << 12)])
+def test_depth_beyond_one_launch_against_oracle(transform, d, b):
+    """d > 63 (the reference accepts any odd d, sketch.py:75-76): compress runs in
+    repetition groups of 63, extraction / queries / heavy hitters read the hash
+    functions from device memory; all against the CPU oracle."""
+    rng = np.random.default_rng(d)
+    n = 160
+    a, m = rng.normal(size=(n, n)), rng.normal(size=(n, n))
+    p = P.SketchParams(n=n, b=b, d=d, transform=transform, seed=77)
+    sk = P.compress(a, m, p)
+    ref = O.compress(a, m, b=b, d=d, transform=transform, seed=77, threads=8)
+    cn = _cnorm(a, m)
+    assert sk.polys.shape == (d, b)
+    assert np.max(np.abs(sk.polys - ref)) <= TOL * cn
+    words = O.draw_words(77, d, b)
+    thr = 0.25 * float(np.abs(a @ m).max())
+    eref, cnt, hh_ref = O.decompress(ref, words, b=b, d=d, transform=transform, n1=n, n2=n, thr=thr, strict=True,
+                                     want_hh=True)
+    est = P.decompress_all(sk)
+    assert np.max(np.abs(est - eref)) <= TOL * cn
+    hh = P.heavy_hitters(sk, thr, strict=True)
+    assert np.array_equal(hh, np.argwhere(np.abs(est) > thr))
+    ij = np.array([[0, 0], [5, 17], [n - 1, n - 1], [80, 3]])
+    q = P.decompress_entries(sk, ij)
+    assert np.array_equal(np.asarray(q), est[ij[:, 0], ij[:, 1]])
+    # the hash tables of every repetition (groups of 63 launches) against the oracle
+    h1, s1, _, _ = O.tables(words, d, b, n, n)
+    assert np.array_equal(_device.hash_table(sk.hashes, 0, n).cpu().numpy().astype(np.int64), h1)
+    assert np.array_equal(_device.hash_table(sk.hashes, 2, n).cpu().numpy().astype(np.float64), s1)

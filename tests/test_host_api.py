@@ -139,7 +139,16 @@ def test_abi_rejects_bad_parameters_before_any_kernel():
     # depth out of range, zero width, bad variant -> SMM_ERR_INVALID (maps to InvalidParameterError);
     # compress accepts even depths (stacked seeds, compress_seeds), extraction does not
     assert lib.smm_compress_workspace(1, 0, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
-    assert lib.smm_compress_workspace(1, 64, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
+    assert lib.smm_compress_workspace(1, _lib.MAX_DEPTH_TOTAL + 1, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_ERR_INVALID
+    # deeper than one launch (groups of 63 repetitions): accepted, same workspace as one group
+    w63, w65 = ctypes.c_int64(0), ctypes.c_int64(0)
+    assert lib.smm_compress_workspace(1, 63, 12, 64, 64, 0, 64, ctypes.byref(w63)) == _lib.SMM_OK
+    assert lib.smm_compress_workspace(1, 65, 12, 64, 64, 0, 64, ctypes.byref(w65)) == _lib.SMM_OK
+    assert w63.value == w65.value > 0
+    # extraction past 63 repetitions carries the hash functions in its workspace
+    assert lib.smm_extract_workspace(63, 8, 8, 0, 8, ctypes.byref(w63)) == _lib.SMM_OK
+    assert lib.smm_extract_workspace(65, 8, 8, 0, 8, ctypes.byref(w65)) == _lib.SMM_OK
+    assert w65.value >= w63.value + 65 * 64
     assert lib.smm_compress_workspace(1, 2, 4, 8, 8, 0, 8, ctypes.byref(out)) == _lib.SMM_OK
     assert lib.smm_extract(1, None, wp, 2, 4, 8, 8, 0, 8, None, 8, 0.5, 1, None, 0, None, None, 0,
                            None) == _lib.SMM_ERR_INVALID
