@@ -33,7 +33,6 @@
 namespace smm {
 
 __global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b);  // fwht2p.cu
-__global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows);
 
 namespace f2p {
 using namespace tp;
@@ -776,10 +775,8 @@ int fft2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   if (nin > 0) {
     csr_fill_fft<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, bs, S1);
     SMM_LAUNCH_CHECK("csr_fill_fft");
-    int64_t sb = ceil_div((int64_t)d * 2 * bs, 256);
-    if (sb > 8192) sb = 8192;
-    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, bs, d * 2);
-    SMM_LAUNCH_CHECK("csr_sort_kernel");
+    const int rc = csr_sort(off, ent, nmax, bs, d * 2, s);  // deterministic: increasing i per bucket
+    if (rc) return rc;
   }
   SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * g.NPU * G2) * 4, s), "counter memset");
   Args p;

@@ -127,25 +127,6 @@ __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const in
   }
 }
 
-// deterministic order inside each bucket: increasing i (the reference's serial order)
-__global__ void csr_sort_kernel(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows) {
-  const int64_t total = (int64_t)rows * b;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = x / b, m = x % b;
-    const int32_t e0 = off[row * (b + 1) + m], e1 = off[row * (b + 1) + m + 1];
-    uint32_t *e = ent + row * nmax;
-    for (int32_t a = e0 + 1; a < e1; ++a) {
-      const uint32_t key = e[a];
-      int32_t q = a - 1;
-      while (q >= e0 && (e[q] & 0x03ffffffu) > (key & 0x03ffffffu)) {
-        e[q + 1] = e[q];
-        --q;
-      }
-      e[q + 1] = key;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ kernel
 // x / d for 0 <= x < 2^31 by multiply-high (the scheduler thread decodes an item
 // on the critical path of every CTA barrier; 32-bit division costs ~20 instructions)
@@ -1121,10 +1102,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   if (nin > 0) {
     csr_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, bs);
     SMM_LAUNCH_CHECK("csr_fill_kernel");
-    int64_t sb = ceil_div((int64_t)d * 2 * bs, 256);
-    if (sb > 8192) sb = 8192;
-    csr_sort_kernel<<<(unsigned)sb, 256, 0, s>>>(off, ent, nmax, bs, d * 2);
-    SMM_LAUNCH_CHECK("csr_sort_kernel");
+    const int rc = csr_sort(off, ent, nmax, bs, d * 2, s);  // deterministic: increasing i per bucket
+    if (rc) return rc;
   }
   SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * F * nblk) * 4, s), "counter memset");
   TwoPassArgs p;

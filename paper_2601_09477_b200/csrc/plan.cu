@@ -338,4 +338,118 @@ int build_plans(const SketchHashes &h, int nops, int64_t n1, int64_t n2, int L, 
   return SMM_OK;
 }
 
+// ------------------------------------------------------------------ CSR bucket sort
+// The CSR fills (fwht2p / fft2p) place each bucket's entries with atomics, so their
+// order inside a bucket is arbitrary; sorting every bucket segment by input index i
+// (entry bits 0-25) restores the reference's serial order (sketch.py:166-172) and
+// makes the plan deterministic.  Segments of <= 32 entries: one thread, insertion
+// sort.  Longer ones (heavily loaded or degenerate hashes) are sorted by a whole CTA
+// with a bitonic network: in shared memory up to 8192 entries, in place in global
+// memory beyond (all-ascending network with virtual +inf padding, so any length).
+namespace {
+constexpr int SHORT_SEG = 32;
+constexpr int SORT_THREADS = 1024;
+constexpr int SMEM_SEG = 8192;
+constexpr uint32_t IDX_MASK = 0x03ffffffu;
+
+__device__ __forceinline__ void cmpswap(uint32_t *e, int64_t a, int64_t b) {
+  const uint32_t x = e[a], y = e[b];
+  if ((x & IDX_MASK) > (y & IDX_MASK)) {
+    e[a] = y;
+    e[b] = x;
+  }
+}
+
+// ascending bitonic sort of e[0, L) by the index bits, virtual +inf past L; P = pow2 >= L
+__device__ void bitonic_all_ascending(uint32_t *e, int64_t L, int64_t P) {
+  for (int64_t k = 2; k <= P; k <<= 1) {
+    // merge of two sorted runs of k/2 with the partner mirrored: every comparator ascending
+    for (int64_t i = threadIdx.x; i < P / 2; i += blockDim.x) {
+      const int64_t blk = i / (k / 2), pos = i % (k / 2);
+      const int64_t a = blk * k + pos, b = blk * k + k - 1 - pos;
+      if (b < L) cmpswap(e, a, b);
+    }
+    __syncthreads();
+    for (int64_t j = k / 4; j >= 1; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        const int64_t a = (i / j) * 2 * j + (i % j), b = a + j;
+        if (b < L) cmpswap(e, a, b);
+      }
+      __syncthreads();
+    }
+  }
+}
+}  // namespace
+
+__global__ void csr_sort_short_kernel(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows) {
+  const int64_t total = (int64_t)rows * b;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = x / b, m = x % b;
+    const int32_t e0 = off[row * (b + 1) + m], e1 = off[row * (b + 1) + m + 1];
+    if (e1 - e0 > SHORT_SEG) continue;  // csr_sort_long_kernel
+    uint32_t *e = ent + row * nmax;
+    for (int32_t a = e0 + 1; a < e1; ++a) {
+      const uint32_t key = e[a];
+      int32_t q = a - 1;
+      while (q >= e0 && (e[q] & IDX_MASK) > (key & IDX_MASK)) {
+        e[q + 1] = e[q];
+        --q;
+      }
+      e[q + 1] = key;
+    }
+  }
+}
+
+// every CTA scans a grid-strided share of the buckets; the long segments it finds
+// are queued in shared memory and sorted one after the other by the whole CTA
+__global__ void __launch_bounds__(SORT_THREADS) csr_sort_long_kernel(const int32_t *off, uint32_t *ent, int64_t nmax,
+                                                                     int64_t b, int rows) {
+  __shared__ uint32_t s_seg[SMEM_SEG];
+  __shared__ int64_t s_q[SORT_THREADS];
+  __shared__ int s_nq;
+  const int64_t total = (int64_t)rows * b;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_nq = 0;
+    __syncthreads();
+    const int64_t x = base + threadIdx.x;
+    if (x < total) {
+      const int64_t row = x / b, m = x % b;
+      if (off[row * (b + 1) + m + 1] - off[row * (b + 1) + m] > SHORT_SEG) s_q[atomicAdd(&s_nq, 1)] = x;
+    }
+    __syncthreads();
+    const int nq = s_nq;
+    for (int q = 0; q < nq; ++q) {
+      const int64_t row = s_q[q] / b, m = s_q[q] % b;
+      const int32_t e0 = off[row * (b + 1) + m], e1 = off[row * (b + 1) + m + 1];
+      const int64_t L = e1 - e0;
+      int64_t P = 1;
+      while (P < L) P <<= 1;
+      uint32_t *e = ent + row * nmax + e0;
+      if (L <= SMEM_SEG) {
+        for (int64_t i = threadIdx.x; i < L; i += blockDim.x) s_seg[i] = e[i];
+        __syncthreads();
+        bitonic_all_ascending(s_seg, L, P);
+        for (int64_t i = threadIdx.x; i < L; i += blockDim.x) e[i] = s_seg[i];
+      } else {
+        bitonic_all_ascending(e, L, P);  // global memory, visible CTA-wide at each barrier
+      }
+      __syncthreads();
+    }
+  }
+}
+
+int csr_sort(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows, cudaStream_t s) {
+  const int64_t total = (int64_t)rows * b;
+  if (total <= 0) return SMM_OK;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > 8192) blocks = 8192;
+  csr_sort_short_kernel<<<(unsigned)blocks, 256, 0, s>>>(off, ent, nmax, b, rows);
+  SMM_LAUNCH_CHECK("csr_sort_short_kernel");
+  int64_t lb = ceil_div(total, SORT_THREADS);
+  if (lb > 2 * num_sms()) lb = 2 * num_sms();
+  csr_sort_long_kernel<<<(unsigned)lb, SORT_THREADS, 0, s>>>(off, ent, nmax, b, rows);
+  SMM_LAUNCH_CHECK("csr_sort_long_kernel");
+  return SMM_OK;
+}
+
 }  // namespace smm

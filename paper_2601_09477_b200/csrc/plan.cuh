@@ -28,6 +28,11 @@ struct PlanView {
 int64_t plan_bytes_per(int64_t nin_max, int L);
 int64_t plan_total_bytes(int d, int nops, int64_t n1, int64_t n2, int L);
 
+// Sorts every bucket segment [off[m], off[m+1]) of `rows` CSR rows of ent (row stride
+// nmax, b buckets, off row stride b + 1) by input index (entry bits 0-25): the
+// deterministic within-bucket order after an atomic fill (plan.cu).
+int csr_sort(const int32_t *off, uint32_t *ent, int64_t nmax, int64_t b, int rows, cudaStream_t s);
+
 // builds all d * nops plans; scratch must hold plan_total_bytes(...)
 int build_plans(const SketchHashes &h, int nops, int64_t n1, int64_t n2, int L, char *ws,
                 cudaStream_t stream);

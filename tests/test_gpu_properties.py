@@ -18,8 +18,10 @@ classes (pkg/tests/test_sketch.py) restated against this implementation:
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2601_09477_b200 as P
+from oracle import sketch_oracle as O
 from paper_2601_09477_b200.hashing import SketchHashes, eval_bucket, eval_sign
 
 pytestmark = pytest.mark.gpu
@@ -178,3 +180,60 @@ def test_nan_propagates_like_np_median():
     a[3, 5] = np.nan
     est = P.decompress_all(P.compress(a, m, p))
     assert np.isnan(est).all()
+
+
+def test_guard_regions_untouched_and_runs_bit_reproducible():
+    """Stand-in for compute-sanitizer memcheck (closed on this GPU pool): every buffer
+    the C ABI writes (accumulator, polys, estimates, pair list, workspaces) sits
+    between 64 KB guard zones of a sentinel pattern inside one allocation; after
+    compress, finalize, extraction and the pair write the guards must be intact.
+    Repeated runs must be bit-identical (a race would show up as run-to-run drift)."""
+    import ctypes
+
+    from paper_2601_09477_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(2)
+    n = 700
+    a = torch.as_tensor(rng.standard_normal((n, n)), device="cuda")
+    bt = torch.as_tensor(rng.standard_normal((n, n)), device="cuda")
+    G = 1 << 16
+    for tr, log2b, d in (("fwht", 12, 3), ("fwht", 16, 5), ("fwht", 17, 3), ("fft", 12, 3), ("fft", 15, 3),
+                         ("fwht", 6, 3), ("fft", 6, 3), ("fwht", 9, 65)):
+        b = 1 << log2b
+        v = _lib.VARIANT[tr]
+        words = O.draw_words(9, d, b)
+        wp = words.ctypes.data_as(ctypes.c_void_p)
+        nb = ctypes.c_int64(0)
+        _lib.check(lib.smm_compress_workspace_ex(v, d, log2b, n, n, 0, n, 1, 1, ctypes.byref(nb)))
+        xb = ctypes.c_int64(0)
+        _lib.check(lib.smm_extract_workspace(d, n, n, 0, n, ctypes.byref(xb)))
+        acc_bytes = d * b * 8 if tr == "fwht" else d * (b // 2 + 1) * 16
+        sizes = [acc_bytes, d * b * 8, n * n * 8, n * n * 16, nb.value, xb.value, 8]
+        offs, pos = [], G
+        for sz in sizes:
+            offs.append(pos)
+            pos += -(-sz // 256) * 256 + G
+        buf = torch.full((pos,), 0xA5, dtype=torch.uint8, device="cuda")
+        base = buf.data_ptr()
+        p = [ctypes.c_void_p(base + o) for o in offs]
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        outs = []
+        for _ in range(3):
+            _lib.check(lib.smm_compress_accumulate_ex(v, ctypes.c_void_p(a.data_ptr()), n, 1,
+                                                      ctypes.c_void_p(bt.data_ptr()), n, 1, n, n, 0, n, wp, d,
+                                                      log2b, p[0], p[4], nb.value, stream))
+            _lib.check(lib.smm_finalize(v, p[0], p[1], d, log2b, stream))
+            if d % 2:
+                _lib.check(lib.smm_extract(v, p[1], wp, d, log2b, n, n, 0, n, p[2], n, 1.0, 1, p[3], n * n, p[6],
+                                           p[5], xb.value, stream))
+            torch.cuda.synchronize()
+            outs.append(buf.clone())
+        guard = torch.ones(pos, dtype=torch.bool, device="cuda")
+        for o, sz in zip(offs, sizes):
+            guard[o:o + sz] = False
+        assert bool((buf[guard] == 0xA5).all()), (tr, log2b, d)
+        # written regions identical across runs (workspaces excluded: scratch)
+        for o, sz in zip(offs[:4] + offs[6:], sizes[:4] + sizes[6:]):
+            assert torch.equal(outs[0][o:o + sz], outs[1][o:o + sz]) and torch.equal(outs[0][o:o + sz],
+                                                                                     outs[2][o:o + sz]), (tr, log2b)
