@@ -991,12 +991,11 @@ static inline int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
 constexpr int MAX_LB = 16;  // per-slice transform bits handled by the two passes (8 + 8)
 
-// Chosen when it is the faster kernel: with more inputs than buckets (b < n) the
-// gather dominates and the fold kernels' row-streaming scatter wins (cfg5 b=2^12,
-// n=8192: 4.2 ms vs 7.3 ms); from b = 2^16 on the two-pass kernel always wins.
+// The two-pass kernel serves every 2^8 <= b <= 2^20 (b > 2^16 through the top-level
+// fold) at any input count below 2^26 (26-bit entry indices); it measured faster than
+// the v1 fold kernels (fwht_compress.cu) at every such width and density, so those
+// only serve b < 2^8 and b > 2^20.
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2) {
-  const int64_t nmax = n1 > n2 ? n1 : n2;
-  (void)nmax;
   return log2b >= P1_BITS && log2b <= MAX_LB + 4 && n1 < ((int64_t)1 << 26) && n2 < ((int64_t)1 << 26);
 }
 

@@ -6,7 +6,7 @@ the FP64 roofline fraction of compress against the measured pipe peak, and the
 CPU oracle (the bit-exact port of the reference algorithm, all host threads) on
 a bounded k-slice / row-slice of the same instance, extrapolated.
 
-    python tools/config_bench.py [cfg ...]  ->  profiles/r01_configs.{json,md}
+    python tools/config_bench.py [cfg ...]  ->  profiles/<round>_configs.{json,md}  (SMM_ROUND, default r02)
     python tools/config_bench.py --from-log LOG   (tables from a run's printed JSON lines)
 """
 import json
@@ -21,7 +21,9 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import paper_2601_09477_b200 as P  # noqa: E402
 from oracle import sketch_oracle as O  # noqa: E402
-from paper_2601_09477_b200 import workloads as W  # noqa: E402
+from paper_2601_09477_b200 import _device, workloads as W  # noqa: E402
+
+ROUND = __import__("os").environ.get("SMM_ROUND", "r02")
 
 FP64_OPS_PEAK = 18.52e12  # DADD / DFMA per second (profiles/r01_microbench.txt)
 DEFAULT = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_b12_d3_nnz512_fwht", "cfg5_b12_d5_nnz512_fft",
@@ -44,7 +46,10 @@ def gpu_times(w, reps=5):
     p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
     est = torch.empty((w.n, w.n), dtype=torch.float64, device="cuda")
     tc, tx = [], []
-    for _ in range(reps + 1):
+    _device.kernel_timing_read(0), _device.kernel_timing_read(1)
+    for i in range(reps + 1):
+        if i == 1:
+            _device.kernel_timing(True)  # the compress kernel's own launches (fwht2p / fft2p), warm runs only
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
         sk = P.compress(w.a, w.bmat, p)
@@ -54,7 +59,26 @@ def gpu_times(w, reps=5):
         torch.cuda.synchronize()
         tc.append(e0.elapsed_time(e1))
         tx.append(e1.elapsed_time(e2))
-    return float(np.median(tc[1:])), float(np.median(tx[1:])), int(pairs.shape[0]), sk
+    _device.kernel_timing(False)
+    ktot, kn = _device.kernel_timing_read(0)
+    _device.kernel_timing_read(1)
+    return float(np.median(tc[1:])), float(np.median(tx[1:])), int(pairs.shape[0]), sk, ktot / max(kn, 1)
+
+
+def dgemm_ms(w):
+    """cuBLAS DGEMM (torch.matmul float64) of the same A, B: context only."""
+    if w.n > 16384:
+        return None
+    c = torch.matmul(w.a, w.bmat)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(2):
+        c = torch.matmul(w.a, w.bmat)
+    e1.record()
+    torch.cuda.synchronize()
+    del c
+    return e0.elapsed_time(e1) / 2
 
 
 def cpu_time(w, threads, budget_s=6.0):
@@ -85,12 +109,14 @@ def main(names):
     rows = []
     for name in names:
         w = W.make(name, xp=torch, device="cuda")
-        tcomp, text, hh, sk = gpu_times(w)
+        tcomp, text, hh, sk, tkern = gpu_times(w)
         ops = fp64_ops(w.n, w.b, w.d, w.transform)
         cpu_ms, ks, rs = cpu_time(w, threads)
+        gemm = dgemm_ms(w)
         row = {"config": name, "n": w.n, "b": w.b, "d": w.d, "transform": w.transform,
-               "compress_ms": tcomp, "extract_ms": text, "total_ms": tcomp + text, "heavy_hitters": hh,
-               "fp64_ops": ops, "fp64_frac": ops / (tcomp * 1e-3) / FP64_OPS_PEAK,
+               "compress_ms": tcomp, "compress_kernel_ms": tkern, "extract_ms": text, "total_ms": tcomp + text,
+               "heavy_hitters": hh, "fp64_ops": ops, "fp64_frac": ops / (tcomp * 1e-3) / FP64_OPS_PEAK,
+               "fp64_frac_kernel": ops / (tkern * 1e-3) / FP64_OPS_PEAK, "dgemm_ms": gemm,
                "extract_write_gbs": 8 * w.n * w.n / (text * 1e-3) / 1e9,
                "cpu_oracle_ms": cpu_ms, "cpu_threads": threads, "cpu_sample": f"k {ks}/{w.n}, rows {rs}/{w.n}",
                "speedup_vs_cpu": cpu_ms / (tcomp + text)}
@@ -102,21 +128,28 @@ def main(names):
 
 
 def write_tables(rows):
-    out = ROOT / "profiles" / "r01_configs.json"
+    out = ROOT / "profiles" / f"{ROUND}_configs.json"
     out.write_text(json.dumps(rows, indent=1))
-    lines = ["| config | transform | n | b | d | compress ms | FP64 frac | extract ms | est. write GB/s | "
-             "CPU oracle ms (threads) | speed-up |", "|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| config | transform | n | b | d | compress ms (kernel) | FP64 frac (kernel) | extract ms | "
+             "est. write GB/s | CPU oracle ms (threads) | speed-up | DGEMM ms (context) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
+        gemm = f"{r['dgemm_ms']:.1f}" if r.get("dgemm_ms") else "-"
         lines.append(f"| {r['config']} | {r['transform']} | {r['n']} | 2^{r['b'].bit_length() - 1} | {r['d']} | "
-                     f"{r['compress_ms']:.2f} | {100 * r['fp64_frac']:.1f} % | {r['extract_ms']:.2f} | "
+                     f"{r['compress_ms']:.2f} ({r.get('compress_kernel_ms', float('nan')):.2f}) | "
+                     f"{100 * r['fp64_frac']:.1f} % ({100 * r.get('fp64_frac_kernel', float('nan')):.1f} %) | "
+                     f"{r['extract_ms']:.2f} | "
                      f"{r['extract_write_gbs']:.0f} | {r['cpu_oracle_ms']:.0f} ({r['cpu_threads']}) | "
-                     f"{r['speedup_vs_cpu']:.0f}x |")
-    (ROOT / "profiles" / "r01_configs.md").write_text(
-        "# Round-1 per-configuration measurements (B200, one GPU)\n\n"
-        "Device time with inputs resident (CUDA events, median of 5); FP64 fraction against the measured\n"
+                     f"{r['speedup_vs_cpu']:.0f}x | {gemm} |")
+    (ROOT / "profiles" / f"{ROUND}_configs.md").write_text(
+        f"# {ROUND} per-configuration measurements (B200, one GPU)\n\n"
+        "Device time with inputs resident (CUDA events, median of 5): compress through the API (B-slab\n"
+        "transpose, hash plans, the compress kernel, inverse) and, in parentheses, the compress kernel's own\n"
+        "launches (fwht2p / fft2p, CUDA events on the launching stream); FP64 fraction against the measured\n"
         "18.52 T ops/s pipe peak (FFT: radix-2 butterflies counted as pipe ops); CPU: the bit-exact oracle\n"
         "port of the reference algorithm on all host threads over a bounded k-slice and row-slice of the\n"
-        "same instance, extrapolated (tools/config_bench.py).\n\n" + "\n".join(lines) + "\n")
+        "same instance, extrapolated (tools/config_bench.py); cuBLAS DGEMM of the same A, B as context\n"
+        "(n <= 16384).\n\n" + "\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
