@@ -79,6 +79,16 @@ const char *smm_last_error(void);
 int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int64_t n,
                     uint32_t *buckets_out, int8_t *signs_out, void *stream);
 
+/* Which compress kernel family serves these shapes (SMM_KERNEL_*): repetitions
+ * computed by the same family are bit-identical however they are stacked, which is
+ * how compress_seeds groups seeds (sketch.py:289-302 per seed, experiments.py:216-312). */
+#define SMM_KERNEL_FOLD 0   /* v1 fold kernels (b < 2^8, b > 2^20)           */
+#define SMM_KERNEL_FWHT2P 1 /* two-pass FWHT, 2^8 <= b <= 2^20               */
+#define SMM_KERNEL_FFT2P 2  /* two-pass FFT                                   */
+#define SMM_KERNEL_FWHT1P 3 /* one-pass FWHT, b = 2^12, n1 + n2 <= 16384, d <= 7 */
+int smm_compress_kernel(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
+                        int *kernel);
+
 /* Device workspace (bytes) needed by smm_compress_accumulate for these shapes. */
 int smm_compress_workspace(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0,
                            int64_t k1, int64_t *bytes);

@@ -130,6 +130,14 @@ def compress_accumulate(a: torch.Tensor, b: torch.Tensor, words: np.ndarray, d: 
     return acc
 
 
+def compress_kernel(variant: str, d: int, log2b: int, n1: int, n2: int, m: int) -> int:
+    """The compress kernel family (SMM_KERNEL_*) the library picks for these shapes."""
+    lib = _lib.load()
+    out = ctypes.c_int(-1)
+    _lib.check(lib.smm_compress_kernel(_lib.VARIANT[variant], d, log2b, n1, n2, 0, m, ctypes.byref(out)))
+    return int(out.value)
+
+
 def copy2d(dst: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream) -> None:
     """dst[...] = src for 2-D row-strided views (host or device, any direction) on ``stream``."""
     lib = _lib.load()

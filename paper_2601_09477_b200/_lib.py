@@ -30,6 +30,7 @@ EXPORTS = (
     "smm_abi_version",
     "smm_last_error",
     "smm_hash_tables",
+    "smm_compress_kernel",
     "smm_compress_workspace",
     "smm_compress_accumulate",
     "smm_compress_workspace_ex",
@@ -78,6 +79,7 @@ def load():
             "smm_abi_version": ([], I),
             "smm_last_error": ([], ctypes.c_char_p),
             "smm_hash_tables": ([P, I, I, I, I64, P, P, P], I),
+            "smm_compress_kernel": ([I, I, I, I64, I64, I64, I64, P], I),
             "smm_compress_workspace": ([I, I, I, I64, I64, I64, I64, P], I),
             "smm_compress_accumulate": ([I, P, I64, P, I64, I64, I64, I64, I64, P, I, I, P, P, I64, P], I),
             "smm_compress_workspace_ex": ([I, I, I, I64, I64, I64, I64, I, I, P], I),

@@ -1,0 +1,449 @@
+// FWHT compress (steps 1-3) for b = 2^12 with small operands (n1 + n2 <= 16384):
+// one pass, one inner index at a time per CTA, everything on chip.
+// Reference: sketch.py:152-189 (scatter :166-172, FWHT :168 / :173, product :176-177).
+//
+// Why a second kernel.  For small transforms the two-pass kernel (fwht2p.cu) is bound
+// by its cross-CTA dependencies: every unit's pass 2 waits for all of its pass 1, and the
+// accumulator of each slice is a chain over the k-tiles.  Here one CTA per SM owns a
+// share of the inner-dimension tiles and keeps everything of one inner index k on chip:
+//   * the two input columns X_A[k, :] (A^T row k) and X_B[k, :] (B row k) are copied
+//     into shared memory with cp.async (n1 + n2 doubles, <= 128 KB) — the signed
+//     scatter then gathers from shared memory instead of L2;
+//   * the CTA's two halves (256 threads each) transform the two operands side by side:
+//     CSR pull into thread-private cells (bucket order = increasing input index, the
+//     reference's serial order), 4 butterfly stages in registers, a swizzled shared-
+//     memory exchange, 4 more, a second exchange, the last 4 (stages in ascending bit
+//     order, as fwht_serial: the transform of one (k, t, op) is bit-identical to the
+//     reference's and to fwht2p's);
+//   * operand A's transform crosses to operand B's half through tensor memory (warps w
+//     and w + 8 share a TMEM lane quadrant), B's half multiplies and extends the tile's
+//     accumulator, which lives in TMEM for all d repetitions (d <= 7);
+//   * the column of k + 1 is copied while the last repetition of k is transformed.
+// The accumulator of every W-wide tile of inner indices (W | 32, relative to the call's
+// k0) is written to a partial buffer; fwht1p_reduce_kernel adds the tiles in k order:
+// acc = ((acc + T0) + T1) + ...  Deterministic, and with k-slabs on multiples of 32 the
+// host-streamed path (SMM_FLAG_ACCUMULATE) reproduces one call's bits.
+#include "plan.cuh"
+#include "twopass.cuh"
+
+namespace smm {
+
+__global__ void csr_count_kernel(SketchHashes h, int64_t n1, int64_t n2, int32_t *cnt, int64_t b);  // fwht2p.cu
+__global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b);
+__global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const int32_t *off, int32_t *fill,
+                                uint32_t *ent, int64_t nmax, int64_t b);
+
+namespace f1p {
+using namespace tp;
+
+constexpr int LB = 12;
+constexpr int B = 1 << LB;
+constexpr int HT = 256;                     // threads per half (one operand each)
+constexpr int CT = 2 * HT;                  // threads per CTA
+constexpr int MAXD = 7;                     // TMEM: 64 columns for A's transform + 64 per repetition
+constexpr int64_t MAX_COLS = 16384;         // n1 + n2 staged in shared memory
+constexpr uint32_t SENT = 0xffffffffu;      // padding entry of the warp-interleaved CSR
+constexpr int WARPS_PER_HALF = HT / 32;
+
+// warp-interleaved CSR (one per (t, op)): entry q of lane l of half-warp w at
+// ent2[base[w] + q * 32 + l], padded to the warp's longest range with SENT, so every
+// step of a warp's scatter loop is one coalesced 128-byte load
+struct Tab {
+  int32_t base, maxcnt;
+};
+
+struct Args {
+  const double *X[2];  // element (input i, inner index k) of operand op at X[op][k * ks[op] + i * is[op]]
+  int64_t ks[2], is[2];
+  int n[2];
+  int64_t K;
+  int d, W, ntiles;
+  const uint32_t *ent2;  // [d][2][...] at row offsets roff[t * 2 + op]
+  int64_t roff[2 * MAXD];
+  const Tab *tab;        // [d][2][8]
+  double *part;          // [ntiles][d][B]
+  int vec16;             // both operands allow 16-byte async copies
+};
+
+// exchange layout: one pad double per 16 (every access pattern below is conflict-free,
+// and a thread's 16 addresses of one access differ by compile-time constants)
+constexpr int XS = B + B / 16;  // doubles per half's exchange area
+__device__ __forceinline__ int swz(int u) { return u + (u >> 4); }
+
+__device__ __forceinline__ void bar_half(int h) { asm volatile("bar.sync %0, 256;" ::"r"(1 + h) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void bar_wait(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
+
+__device__ __forceinline__ void fwht16(double (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int hq = 1 << q;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (!(j & hq)) {
+        const double x = v[j], y = v[j + hq];
+        v[j] = x + y;
+        v[j + hq] = x - y;
+      }
+  }
+}
+
+// copy column k of operand h into shared memory (cp.async, no registers).  A k-minor
+// operand (A row-major) is read with 8-byte copies at stride is: 4x the L2 sectors, but
+// the neighbouring inner indices of each sector are the CTA's next columns (L2 hits), and
+// no transposed copy of the operand is needed
+__device__ __forceinline__ void column_copy(const Args &p, int h, int64_t k, double *col, int ht) {
+  const double *src = p.X[h] + k * p.ks[h];
+  const int n = p.n[h];
+  if (p.is[h] != 1) {
+    const int64_t st = p.is[h];
+    for (int i = ht; i < n; i += HT) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(col + i);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + i * st) : "memory");
+    }
+  } else if (p.vec16 & (1 << h)) {
+    for (int i = 2 * ht; i < n; i += 2 * HT) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(col + i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + i) : "memory");
+    }
+  } else {
+    for (int i = ht; i < n; i += HT) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(col + i);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + i) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int h = tid >> 8;   // 0: operand A, 1: operand B
+  const int ht = tid & 255;
+  const int hw = ht >> 5;   // warp within the half
+  double *X = sm + h * XS;  // this half's exchange area (34 KB)
+  double *col = sm + 2 * XS + (h ? p.n[0] : 0);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+  const uint32_t col_fa = (uint32_t)((hw >> 2) * 32);                     // A's transform
+  auto col_acc = [&](int t) { return (uint32_t)(64 + t * 64 + (hw >> 2) * 32); };  // tile accumulator of t
+  const int d = p.d;
+  bool fa_pending = false;  // half A: B's half has not yet consumed the previous transform
+  int64_t tile = blockIdx.x;
+  int64_t k = tile * p.W;
+  if (tile < p.ntiles) column_copy(p, h, k, col, ht);
+  for (; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t k_lo = tile * p.W;
+    const int64_t k_hi = k_lo + p.W < p.K ? k_lo + p.W : p.K;
+    for (k = k_lo; k < k_hi; ++k) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      bar_half(h);  // the column is visible to the whole half; the exchange area is free
+      for (int t = 0; t < d; ++t) {
+        // ---- signed scatter of column k into this thread's 16 buckets [16 ht, 16 ht + 16)
+        const Tab tb = p.tab[(t * 2 + h) * WARPS_PER_HALF + hw];
+        const uint32_t *e2 = p.ent2 + p.roff[t * 2 + h] + tb.base + lane;
+        uint32_t mask = 0;
+        int cur = -1;
+        double run = 0.0;
+        // batches of 8 entry words, the next batch's loads in flight while this one is added;
+        // a bucket's sum is stored when the next bucket starts (predicated, no branches)
+        uint32_t wn[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) wn[r] = r < tb.maxcnt ? __ldg(e2 + r * 32) : SENT;
+        for (int q0 = 0; q0 < tb.maxcnt; q0 += 8) {
+          uint32_t w[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            w[r] = wn[r];
+            wn[r] = q0 + 8 + r < tb.maxcnt ? __ldg(e2 + (q0 + 8 + r) * 32) : SENT;
+          }
+          double x[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) x[r] = w[r] != SENT ? col[w[r] & 0x03ffffffu] : 0.0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const double val = (w[r] >> 31) ? -x[r] : x[r];  // s(i) * a (sketch.py:166-167)
+            const int j = (int)((w[r] >> 26) & 15u);
+            const double nr = j == cur ? run + val : 0.0 + val;  // the reference's buckets start at 0.0
+            if (w[r] != SENT) {
+              if (j != cur && cur >= 0) X[swz(16 * ht + cur)] = run;  // the previous bucket is complete
+              run = nr;
+              cur = j;
+              mask |= 1u << j;
+            }
+          }
+        }
+        if (cur >= 0) X[swz(16 * ht + cur)] = run;
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? X[swz(16 * ht + j)] : 0.0;
+        if (t == d - 1) {
+          // every gather of column k done by the half: copy column k + 1 while k finishes
+          bar_half(h);
+          int64_t kn = k + 1;
+          if (kn >= k_hi) {
+            const int64_t tn = tile + gridDim.x;
+            kn = tn < p.ntiles ? tn * p.W : -1;
+          }
+          if (kn >= 0) column_copy(p, h, kn, col, ht);
+        }
+        // ---- FWHT over the 12 bucket bits, ascending (fwht_serial's stage order)
+        fwht16(v);  // bits 0-3
+#pragma unroll
+        for (int j = 0; j < 16; ++j) X[swz(16 * ht + j)] = v[j];
+        bar_half(h);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = X[swz((ht & 15) | (j << 4) | ((ht >> 4) << 8))];
+        fwht16(v);  // bits 4-7
+        bar_half(h);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) X[swz((ht & 15) | (j << 4) | ((ht >> 4) << 8))] = v[j];
+        bar_half(h);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = X[swz(ht | (j << 8))];
+        fwht16(v);  // bits 8-11: thread holds buckets ht | j << 8
+        // ---- product through TMEM
+        if (h == 0) {
+          if (fa_pending) {
+            bar_wait(4);  // B's half has loaded the previous transform
+            tc_fence_after();
+          }
+          tmem_st8(tq + col_fa, v);
+          tmem_st8(tq + col_fa + 16, v + 8);
+          tmem_wait_st();
+          tc_fence_before();
+          bar_arrive(3);
+          fa_pending = true;
+        } else {
+          bar_wait(3);
+          tc_fence_after();
+          double fa[16];
+          tmem_ld8(tq + col_fa, fa);
+          tmem_ld8(tq + col_fa + 16, fa + 8);
+          tc_fence_before();
+          bar_arrive(4);
+          double pr[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pr[j] = __dmul_rn(fa[j], v[j]);  // partial += pa * pb (sketch.py:176-177)
+          if (k > k_lo) {
+            double acc[16];
+            tmem_ld8(tq + col_acc(t), acc);
+            tmem_ld8(tq + col_acc(t) + 16, acc + 8);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pr[j] = __dadd_rn(acc[j], pr[j]);
+          }
+          tmem_st8(tq + col_acc(t), pr);
+          tmem_st8(tq + col_acc(t) + 16, pr + 8);
+          tmem_wait_st();
+        }
+        bar_half(h);  // the exchange area is reused by the next repetition's scatter
+      }
+    }
+    // ---- the tile's sums to the partial buffer (B's half owns the accumulators)
+    if (h == 1) {
+      for (int t = 0; t < d; ++t) {
+        double acc[16];
+        tmem_ld8(tq + col_acc(t), acc);
+        tmem_ld8(tq + col_acc(t) + 16, acc + 8);
+        double *dst = p.part + ((int64_t)tile * d + t) * B + ht;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcs(dst + (j << 8), acc[j]);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (h == 0 && fa_pending) bar_wait(4);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// acc[t][u] = ((acc_in + T0) + T1) + ... over the tiles in k order (acc_add), or from T0
+__global__ void fwht1p_reduce_kernel(const double *part, int ntiles, int d, double *acc, int acc_add) {
+  const int64_t total = (int64_t)d * B;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = x / B, u = x % B;
+    const double *pt = part + t * B + u;
+    const int64_t stride = (int64_t)d * B;
+    double s = acc_add ? acc[x] + pt[0] : pt[0];
+    // batches of 32 independent loads, then the additions in tile order (few threads: d x b)
+    for (int q0 = 1; q0 < ntiles; q0 += 32) {
+      double v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = q0 + r < ntiles ? __ldcg(pt + (int64_t)(q0 + r) * stride) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (q0 + r < ntiles) s += v[r];
+    }
+    acc[x] = s;
+  }
+}
+
+// warp-interleaved CSR of one (t, op) row per block (256 threads = the 8 warps of a half)
+struct RowOffsets {
+  int64_t r[2 * MAXD];
+};
+__global__ void csr_interleave_kernel(const int32_t *off, const uint32_t *ent, int64_t nmax, uint32_t *ent2,
+                                      RowOffsets roff, Tab *tab) {
+  __shared__ int s_max[WARPS_PER_HALF];
+  const int row = blockIdx.x;
+  const int ht = threadIdx.x, hw = ht >> 5, lane = ht & 31;
+  const int32_t *o = off + (int64_t)row * (B + 1);
+  const int lo = o[16 * ht], hi = o[16 * ht + 16];
+  const int cnt = hi - lo;
+  const int mx = __reduce_max_sync(0xffffffffu, cnt);
+  if (lane == 0) s_max[hw] = mx;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < hw; ++w) base += 32 * s_max[w];
+  if (lane == 0) tab[row * WARPS_PER_HALF + hw] = Tab{base, mx};
+  uint32_t *dst = ent2 + roff.r[row] + base + lane;
+  const uint32_t *src = ent + (int64_t)row * nmax + lo;
+  for (int q = 0; q < mx; ++q) dst[q * 32] = q < cnt ? src[q] : SENT;
+}
+
+// words of one interleaved row: the sum over the 8 warps of 32 x (their longest range) is at
+// most 32 x (the row's entries)
+static int64_t ent2_row_bound(int64_t nop) { return 32 * (nop > 0 ? nop : 1); }
+
+}  // namespace f1p
+
+static inline int64_t pad256_(int64_t x) { return ((x + 255) / 256) * 256; }
+
+static int f1p_tile_width(int d, int64_t K) {
+  // W | 32: the finest that keeps the partial buffer under 512 MB (load balance over the SMs)
+  for (int W : {8, 16, 32}) {
+    const int64_t nt = (K + W - 1) / W;
+    if (nt * d * f1p::B * 8 <= ((int64_t)512 << 20)) return W;
+  }
+  return 0;
+}
+
+bool fwht1p_supported(int log2b, int d, int64_t n1, int64_t n2, int64_t K) {
+  static const bool off = getenv("SMM_NO_FWHT1P") != nullptr;
+  return !off && log2b == f1p::LB && d >= 1 && d <= f1p::MAXD && n1 + n2 <= f1p::MAX_COLS && n1 < (1 << 26) &&
+         n2 < (1 << 26) && (K == 0 || f1p_tile_width(d, K) > 0);
+}
+
+int64_t fwht1p_workspace(int d, int64_t n1, int64_t n2, int64_t K) {
+  using namespace f1p;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  const int W = f1p_tile_width(d, K > 0 ? K : 1);
+  const int64_t nt = (K + (W ? W : 32) - 1) / (W ? W : 32);
+  int64_t w = 0;
+  w += pad256_((int64_t)d * 2 * (B + 1) * 4);  // off
+  w += pad256_((int64_t)d * 2 * B * 4);        // cnt / fill
+  w += pad256_((int64_t)d * 2 * nmax * 4);     // ent
+  w += pad256_((int64_t)d * (ent2_row_bound(n1) + ent2_row_bound(n2)) * 4);  // ent2
+  w += pad256_((int64_t)d * 2 * WARPS_PER_HALF * sizeof(Tab));
+  w += pad256_(nt * d * B * 8);                // partial tile sums
+  return w;
+}
+
+// operands in either layout (a_kminor / b_kminor: row = input, inner index contiguous;
+// else row = inner index); inner range [k0, k1)
+int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool a_kminor, const double *xb,
+                      int64_t ldb, bool b_kminor, int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc,
+                      bool acc_add, char *ws, int64_t ws_bytes, cudaStream_t s) {
+  using namespace f1p;
+  const int d = h.d;
+  const int64_t K = k1 - k0;
+  const int64_t nmax = n1 > n2 ? n1 : n2;
+  if (ws_bytes < fwht1p_workspace(d, n1, n2, K)) {
+    set_error("compress workspace too small (one-pass)");
+    return SMM_ERR_WORKSPACE;
+  }
+  if (K <= 0) {
+    if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * B * 8, s), "acc memset");
+    return SMM_OK;
+  }
+  const int W = f1p_tile_width(d, K);
+  const int64_t nt = (K + W - 1) / W;
+  char *q = ws;
+  int32_t *off = (int32_t *)q;
+  q += pad256_((int64_t)d * 2 * (B + 1) * 4);
+  int32_t *cnt = (int32_t *)q;
+  q += pad256_((int64_t)d * 2 * B * 4);
+  uint32_t *ent = (uint32_t *)q;
+  q += pad256_((int64_t)d * 2 * nmax * 4);
+  uint32_t *ent2 = (uint32_t *)q;
+  q += pad256_((int64_t)d * (ent2_row_bound(n1) + ent2_row_bound(n2)) * 4);
+  Tab *tab = (Tab *)q;
+  q += pad256_((int64_t)d * 2 * WARPS_PER_HALF * sizeof(Tab));
+  double *part = (double *)q;
+  // CSR by bucket (fwht2p.cu's plan kernels) and its warp-interleaved copy
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * B * 4, s), "csr memset");
+  const int64_t nin = (int64_t)d * (n1 + n2);
+  int64_t blocks = ceil_div(nin, 256);
+  if (blocks > 8192) blocks = 8192;
+  if (nin > 0) {
+    csr_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, cnt, B);
+    SMM_LAUNCH_CHECK("csr_count_kernel");
+  }
+  csr_scan_kernel<<<d * 2, 1024, 0, s>>>(cnt, off, B);
+  SMM_LAUNCH_CHECK("csr_scan_kernel");
+  SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * B * 4, s), "csr memset");
+  if (nin > 0) {
+    csr_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(h, n1, n2, off, cnt, ent, nmax, B);
+    SMM_LAUNCH_CHECK("csr_fill_kernel");
+    const int rc = csr_sort(off, ent, nmax, B, d * 2, s);
+    if (rc) return rc;
+  }
+  RowOffsets ro;
+  {
+    int64_t pos = 0;
+    for (int r = 0; r < 2 * d; ++r) {
+      ro.r[r] = pos;
+      pos += ent2_row_bound((r & 1) ? n2 : n1);
+    }
+  }
+  csr_interleave_kernel<<<2 * d, HT, 0, s>>>(off, ent, nmax, ent2, ro, tab);
+  SMM_LAUNCH_CHECK("csr_interleave_kernel");
+  Args p;
+  p.ks[0] = a_kminor ? 1 : lda;
+  p.is[0] = a_kminor ? lda : 1;
+  p.ks[1] = b_kminor ? 1 : ldb;
+  p.is[1] = b_kminor ? ldb : 1;
+  p.X[0] = xa + k0 * p.ks[0];
+  p.X[1] = xb + k0 * p.ks[1];
+  p.n[0] = (int)n1;
+  p.n[1] = (int)n2;
+  p.K = K;
+  p.d = d;
+  p.W = W;
+  p.ntiles = (int)nt;
+  p.ent2 = ent2;
+  for (int r = 0; r < 2 * MAXD; ++r) p.roff[r] = r < 2 * d ? ro.r[r] : 0;
+  p.tab = tab;
+  p.part = part;
+  p.vec16 = 0;  // per operand: 16-byte copies of contiguous columns
+  if (p.is[0] == 1 && p.ks[0] % 2 == 0 && n1 % 2 == 0 && (uintptr_t)p.X[0] % 16 == 0) p.vec16 |= 1;
+  if (p.is[1] == 1 && p.ks[1] % 2 == 0 && n2 % 2 == 0 && (uintptr_t)p.X[1] % 16 == 0) p.vec16 |= 2;
+  const size_t smem = (size_t)(2 * XS + n1 + n2) * 8;
+  SMM_CUDA_TRY(cudaFuncSetAttribute(fwht1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "fwht1p smem");
+  int grid = num_sms();
+  if (grid > nt) grid = (int)nt;
+  {
+    KernelTimer timer(0, s);
+    fwht1p_kernel<<<grid, CT, smem, s>>>(p);
+    timer.stop();
+  }
+  SMM_LAUNCH_CHECK("fwht1p_kernel");
+  fwht1p_reduce_kernel<<<(unsigned)ceil_div((int64_t)d * B, 64), 64, 0, s>>>(part, (int)nt, d, acc, acc_add ? 1 : 0);
+  SMM_LAUNCH_CHECK("fwht1p_reduce_kernel");
+  return SMM_OK;
+}
+
+}  // namespace smm

@@ -333,7 +333,12 @@ def compress_seeds(a, b, params: SketchParams, seeds, threads: int | None = None
     else:
         a_op, b_op = _as_matrix(a, "left operand", dev), _as_matrix(b, "right operand", dev)
     d = params.d
+    # seeds stacked into one launch of the kernel family a single-seed compress would use,
+    # so every sketch is bit-identical to its own compress call
+    single = _device.compress_kernel(params.transform, d, params.log2b, n, n, n)
     group = max(1, MAX_DEPTH // d)
+    while group > 1 and _device.compress_kernel(params.transform, d * group, params.log2b, n, n, n) != single:
+        group -= 1
     out = []
     for g0 in range(0, len(per), group):
         ps = per[g0:g0 + group]

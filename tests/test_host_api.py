@@ -188,3 +188,18 @@ def test_api_validates_before_device_work():
     # valid input without a GPU fails loudly: there is no CPU fallback
     with pytest.raises(RuntimeError):
         P.compress(np.zeros((8, 8)), np.zeros((8, 8)), p)
+
+
+def test_compress_kernel_family_dispatch():
+    """smm_compress_kernel: which kernel family serves a shape (compress_seeds stacks
+    seeds only within one family, so every sketch keeps its single-call bits)."""
+    from paper_2601_09477_b200 import _device
+
+    K = {"fold": 0, "fwht2p": 1, "fft2p": 2, "fwht1p": 3}
+    assert _device.compress_kernel("fwht", 3, 12, 8192, 8192, 8192) == K["fwht1p"]   # cfg5 b = 2^12
+    assert _device.compress_kernel("fwht", 3, 12, 1024, 1024, 1024) == K["fwht1p"]   # cfg1
+    assert _device.compress_kernel("fwht", 9, 12, 8192, 8192, 8192) == K["fwht2p"]   # d > 7: TMEM budget
+    assert _device.compress_kernel("fwht", 3, 12, 16384, 16384, 16384) == K["fwht2p"]  # columns exceed smem
+    assert _device.compress_kernel("fwht", 5, 16, 16384, 16384, 16384) == K["fwht2p"]  # cfg3
+    assert _device.compress_kernel("fft", 5, 14, 4096, 4096, 4096) == K["fft2p"]     # cfg2
+    assert _device.compress_kernel("fwht", 3, 6, 100, 100, 100) == K["fold"]         # b < 2^8
