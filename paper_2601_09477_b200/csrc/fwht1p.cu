@@ -42,12 +42,16 @@ constexpr int HT = 256;                     // threads per half (one operand eac
 constexpr int CT = 2 * HT;                  // threads per CTA
 constexpr int MAXD = 7;                     // TMEM: 64 columns for A's transform + 64 per repetition
 constexpr int64_t MAX_COLS = 16384;         // n1 + n2 staged in shared memory
-constexpr uint32_t SENT = 0xffffffffu;      // padding entry of the warp-interleaved CSR
 constexpr int WARPS_PER_HALF = HT / 32;
+// scatter word of the warp-interleaved CSR: byte offset of input i in the staged column
+// (bits 0-16, i < 16384), bucket j within the thread's 16 (bits 17-20), first / last
+// entry of its bucket (bits 21 / 22), sign (bit 31).  Padding words point at the zero
+// double past the column and carry no flags.
+constexpr uint32_t W_OFF = 0x1ffffu, W_FIRST = 1u << 21, W_LAST = 1u << 22, W_SIGN = 1u << 31;
 
 // warp-interleaved CSR (one per (t, op)): entry q of lane l of half-warp w at
-// ent2[base[w] + q * 32 + l], padded to the warp's longest range with SENT, so every
-// step of a warp's scatter loop is one coalesced 128-byte load
+// ent2[base[w] + q * 32 + l], padded to the warp's longest range, so every step of a
+// warp's scatter loop is one coalesced 128-byte load
 struct Tab {
   int32_t base, maxcnt;
 };
@@ -61,6 +65,7 @@ struct Args {
   const uint32_t *ent2;  // [d][2][...] at row offsets roff[t * 2 + op]
   int64_t roff[2 * MAXD];
   const Tab *tab;        // [d][2][8]
+  const uint32_t *bmask;  // [d][2][256]: buckets of each thread's 16 that have an entry
   double *part;          // [ntiles][d][B]
   int vec16;             // both operands allow 16-byte async copies
 };
@@ -124,7 +129,11 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
   const int ht = tid & 255;
   const int hw = ht >> 5;   // warp within the half
   double *X = sm + h * XS;  // this half's exchange area (34 KB)
-  double *col = sm + 2 * XS + (h ? p.n[0] : 0);
+  // staged columns, each followed by one zero double (the padding words' target)
+  double *col = sm + 2 * XS + (h ? ((p.n[0] + 2) & ~1) : 0);
+  if (ht == 0) col[p.n[h]] = 0.0;
+  const uint32_t col_s = (uint32_t)__cvta_generic_to_shared(col);
+  double *cells = X + 17 * ht;  // this thread's 16 buckets [16 ht, 16 ht + 16) in the padded layout
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_tmem)));
@@ -149,44 +158,40 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       bar_half(h);  // the column is visible to the whole half; the exchange area is free
       for (int t = 0; t < d; ++t) {
-        // ---- signed scatter of column k into this thread's 16 buckets [16 ht, 16 ht + 16)
+        // ---- signed scatter of column k into this thread's 16 buckets [16 ht, 16 ht + 16):
+        // entries in bucket order (increasing input index inside a bucket, the reference's
+        // order); a bucket's sum starts from 0.0 at its first entry and is stored at its last
         const Tab tb = p.tab[(t * 2 + h) * WARPS_PER_HALF + hw];
         const uint32_t *e2 = p.ent2 + p.roff[t * 2 + h] + tb.base + lane;
-        uint32_t mask = 0;
-        int cur = -1;
+        const uint32_t mask = __ldg(p.bmask + (t * 2 + h) * HT + ht);
         double run = 0.0;
-        // batches of 8 entry words, the next batch's loads in flight while this one is added;
-        // a bucket's sum is stored when the next bucket starts (predicated, no branches)
         uint32_t wn[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) wn[r] = r < tb.maxcnt ? __ldg(e2 + r * 32) : SENT;
+        for (int r = 0; r < 8; ++r) wn[r] = r < tb.maxcnt ? __ldg(e2 + r * 32) : (uint32_t)(p.n[h] * 8);
         for (int q0 = 0; q0 < tb.maxcnt; q0 += 8) {
           uint32_t w[8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
+          for (int r = 0; r < 8; ++r) {  // the next batch's words are in flight while this one is added
             w[r] = wn[r];
-            wn[r] = q0 + 8 + r < tb.maxcnt ? __ldg(e2 + (q0 + 8 + r) * 32) : SENT;
+            wn[r] = q0 + 8 + r < tb.maxcnt ? __ldg(e2 + (q0 + 8 + r) * 32) : (uint32_t)(p.n[h] * 8);
           }
           double x[8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) x[r] = w[r] != SENT ? col[w[r] & 0x03ffffffu] : 0.0;
+          for (int r = 0; r < 8; ++r) {
+            double y;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(y) : "r"(col_s + (w[r] & W_OFF)));
+            // s(i) * a (sketch.py:166-167): the sign bit moved into the double's sign
+            x[r] = __hiloint2double(__double2hiint(y) ^ (int)(w[r] & W_SIGN), __double2loint(y));
+          }
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
-            const double val = (w[r] >> 31) ? -x[r] : x[r];  // s(i) * a (sketch.py:166-167)
-            const int j = (int)((w[r] >> 26) & 15u);
-            const double nr = j == cur ? run + val : 0.0 + val;  // the reference's buckets start at 0.0
-            if (w[r] != SENT) {
-              if (j != cur && cur >= 0) X[swz(16 * ht + cur)] = run;  // the previous bucket is complete
-              run = nr;
-              cur = j;
-              mask |= 1u << j;
-            }
+            run = ((w[r] & W_FIRST) ? 0.0 : run) + x[r];  // the reference's buckets start at 0.0
+            if (w[r] & W_LAST) cells[(w[r] >> 17) & 15u] = run;
           }
         }
-        if (cur >= 0) X[swz(16 * ht + cur)] = run;
         double v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? X[swz(16 * ht + j)] : 0.0;
+        for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? cells[j] : 0.0;
         if (t == d - 1) {
           // every gather of column k done by the half: copy column k + 1 while k finishes
           bar_half(h);
@@ -290,14 +295,16 @@ __global__ void fwht1p_reduce_kernel(const double *part, int ntiles, int d, doub
   }
 }
 
-// warp-interleaved CSR of one (t, op) row per block (256 threads = the 8 warps of a half)
 struct RowOffsets {
   int64_t r[2 * MAXD];
 };
+
+// warp-interleaved scatter words of one (t, op) row per block (256 threads = the 8 warps of a half)
 __global__ void csr_interleave_kernel(const int32_t *off, const uint32_t *ent, int64_t nmax, uint32_t *ent2,
-                                      RowOffsets roff, Tab *tab) {
+                                      RowOffsets roff, Tab *tab, uint32_t *bmask, int n0, int n1) {
   __shared__ int s_max[WARPS_PER_HALF];
   const int row = blockIdx.x;
+  const int nop = (row & 1) ? n1 : n0;
   const int ht = threadIdx.x, hw = ht >> 5, lane = ht & 31;
   const int32_t *o = off + (int64_t)row * (B + 1);
   const int lo = o[16 * ht], hi = o[16 * ht + 16];
@@ -310,7 +317,20 @@ __global__ void csr_interleave_kernel(const int32_t *off, const uint32_t *ent, i
   if (lane == 0) tab[row * WARPS_PER_HALF + hw] = Tab{base, mx};
   uint32_t *dst = ent2 + roff.r[row] + base + lane;
   const uint32_t *src = ent + (int64_t)row * nmax + lo;
-  for (int q = 0; q < mx; ++q) dst[q * 32] = q < cnt ? src[q] : SENT;
+  uint32_t mask = 0;
+  for (int q = 0; q < mx; ++q) {
+    uint32_t wd = (uint32_t)nop * 8u;  // padding: the zero double past the column
+    if (q < cnt) {
+      const uint32_t e = src[q];
+      const uint32_t j = (e >> 26) & 15u;
+      const bool first = q == 0 || ((src[q - 1] >> 26) & 15u) != j;
+      const bool last = q == cnt - 1 || ((src[q + 1] >> 26) & 15u) != j;
+      wd = ((e & 0x03ffffffu) * 8u) | (j << 17) | (first ? W_FIRST : 0u) | (last ? W_LAST : 0u) | (e & W_SIGN);
+      mask |= 1u << j;
+    }
+    dst[q * 32] = wd;
+  }
+  bmask[row * HT + ht] = mask;
 }
 
 // words of one interleaved row: the sum over the 8 warps of 32 x (their longest range) is at
@@ -332,8 +352,8 @@ static int f1p_tile_width(int d, int64_t K) {
 
 bool fwht1p_supported(int log2b, int d, int64_t n1, int64_t n2, int64_t K) {
   static const bool off = getenv("SMM_NO_FWHT1P") != nullptr;
-  return !off && log2b == f1p::LB && d >= 1 && d <= f1p::MAXD && n1 + n2 <= f1p::MAX_COLS && n1 < (1 << 26) &&
-         n2 < (1 << 26) && (K == 0 || f1p_tile_width(d, K) > 0);
+  return !off && log2b == f1p::LB && d >= 1 && d <= f1p::MAXD && n1 + n2 <= f1p::MAX_COLS && n1 < f1p::MAX_COLS &&
+         n2 < f1p::MAX_COLS && (K == 0 || f1p_tile_width(d, K) > 0);
 }
 
 int64_t fwht1p_workspace(int d, int64_t n1, int64_t n2, int64_t K) {
@@ -347,6 +367,7 @@ int64_t fwht1p_workspace(int d, int64_t n1, int64_t n2, int64_t K) {
   w += pad256_((int64_t)d * 2 * nmax * 4);     // ent
   w += pad256_((int64_t)d * (ent2_row_bound(n1) + ent2_row_bound(n2)) * 4);  // ent2
   w += pad256_((int64_t)d * 2 * WARPS_PER_HALF * sizeof(Tab));
+  w += pad256_((int64_t)d * 2 * HT * 4);       // bucket masks
   w += pad256_(nt * d * B * 8);                // partial tile sums
   return w;
 }
@@ -381,6 +402,8 @@ int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool
   q += pad256_((int64_t)d * (ent2_row_bound(n1) + ent2_row_bound(n2)) * 4);
   Tab *tab = (Tab *)q;
   q += pad256_((int64_t)d * 2 * WARPS_PER_HALF * sizeof(Tab));
+  uint32_t *bmask = (uint32_t *)q;
+  q += pad256_((int64_t)d * 2 * HT * 4);
   double *part = (double *)q;
   // CSR by bucket (fwht2p.cu's plan kernels) and its warp-interleaved copy
   SMM_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)d * 2 * B * 4, s), "csr memset");
@@ -408,7 +431,7 @@ int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool
       pos += ent2_row_bound((r & 1) ? n2 : n1);
     }
   }
-  csr_interleave_kernel<<<2 * d, HT, 0, s>>>(off, ent, nmax, ent2, ro, tab);
+  csr_interleave_kernel<<<2 * d, HT, 0, s>>>(off, ent, nmax, ent2, ro, tab, bmask, (int)n1, (int)n2);
   SMM_LAUNCH_CHECK("csr_interleave_kernel");
   Args p;
   p.ks[0] = a_kminor ? 1 : lda;
@@ -426,11 +449,12 @@ int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool
   p.ent2 = ent2;
   for (int r = 0; r < 2 * MAXD; ++r) p.roff[r] = r < 2 * d ? ro.r[r] : 0;
   p.tab = tab;
+  p.bmask = bmask;
   p.part = part;
   p.vec16 = 0;  // per operand: 16-byte copies of contiguous columns
   if (p.is[0] == 1 && p.ks[0] % 2 == 0 && n1 % 2 == 0 && (uintptr_t)p.X[0] % 16 == 0) p.vec16 |= 1;
   if (p.is[1] == 1 && p.ks[1] % 2 == 0 && n2 % 2 == 0 && (uintptr_t)p.X[1] % 16 == 0) p.vec16 |= 2;
-  const size_t smem = (size_t)(2 * XS + n1 + n2) * 8;
+  const size_t smem = (size_t)(2 * XS + ((n1 + 2) & ~1) + n2 + 1) * 8;
   SMM_CUDA_TRY(cudaFuncSetAttribute(fwht1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "fwht1p smem");
   int grid = num_sms();
