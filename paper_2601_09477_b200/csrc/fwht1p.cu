@@ -17,7 +17,8 @@
 //     reference's and to fwht2p's);
 //   * operand A's transform crosses to operand B's half through tensor memory (warps w
 //     and w + 8 share a TMEM lane quadrant), B's half multiplies and extends the tile's
-//     accumulator, which lives in TMEM for all d repetitions (d <= 7);
+//     accumulator, which lives in TMEM for all d repetitions (d <= 7; deeper sketches
+//     run as balanced groups of at most 7 repetitions, one launch each);
 //   * the column of k + 1 is copied while the last repetition of k is transformed.
 // The accumulator of every W-wide tile of inner indices (W | 32, relative to the call's
 // k0) is written to a partial buffer; fwht1p_reduce_kernel adds the tiles in k order:
@@ -350,14 +351,24 @@ static int f1p_tile_width(int d, int64_t K) {
   return 0;
 }
 
+// repetitions per launch: up to MAXD (the TMEM accumulators), deeper sketches in balanced
+// groups of at most MAXD, one launch each (cfg5 b = 2^12 d = 9: 4.93 ms through fwht2p,
+// 3.61 ms as two one-pass launches)
+static int f1p_group(int d) {
+  if (d <= f1p::MAXD) return d;
+  const int ng = (d + f1p::MAXD - 1) / f1p::MAXD;
+  return (d + ng - 1) / ng;
+}
+
 bool fwht1p_supported(int log2b, int d, int64_t n1, int64_t n2, int64_t K) {
   static const bool off = getenv("SMM_NO_FWHT1P") != nullptr;
-  return !off && log2b == f1p::LB && d >= 1 && d <= f1p::MAXD && n1 + n2 <= f1p::MAX_COLS && n1 < f1p::MAX_COLS &&
-         n2 < f1p::MAX_COLS && (K == 0 || f1p_tile_width(d, K) > 0);
+  return !off && log2b == f1p::LB && d >= 1 && d <= SMM_MAX_DEPTH && n1 + n2 <= f1p::MAX_COLS &&
+         n1 < f1p::MAX_COLS && n2 < f1p::MAX_COLS && (K == 0 || f1p_tile_width(f1p_group(d), K) > 0);
 }
 
 int64_t fwht1p_workspace(int d, int64_t n1, int64_t n2, int64_t K) {
   using namespace f1p;
+  d = f1p_group(d);  // one group's workspace, reused by the next group
   const int64_t nmax = n1 > n2 ? n1 : n2;
   const int W = f1p_tile_width(d, K > 0 ? K : 1);
   const int64_t nt = (K + (W ? W : 32) - 1) / (W ? W : 32);
@@ -378,6 +389,22 @@ int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool
                       int64_t ldb, bool b_kminor, int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc,
                       bool acc_add, char *ws, int64_t ws_bytes, cudaStream_t s) {
   using namespace f1p;
+  if (h.d > MAXD) {
+    // repetition groups, one launch each, into rows [t0, t0 + dg) of acc (workspace reused;
+    // every repetition is independent, so the bits equal one launch's)
+    const int dg = f1p_group(h.d);
+    for (int t0 = 0; t0 < h.d; t0 += dg) {
+      SketchHashes hg;
+      hg.d = t0 + dg <= h.d ? dg : h.d - t0;
+      hg.log2b = h.log2b;
+      for (int g = 0; g < 4; ++g)
+        for (int t = 0; t < hg.d; ++t) hg.f[g][t] = h.f[g][t0 + t];
+      const int rc = fwht1p_accumulate(hg, xa, lda, a_kminor, xb, ldb, b_kminor, n1, n2, k0, k1,
+                                       acc + (int64_t)t0 * B, acc_add, ws, ws_bytes, s);
+      if (rc) return rc;
+    }
+    return SMM_OK;
+  }
   const int d = h.d;
   const int64_t K = k1 - k0;
   const int64_t nmax = n1 > n2 ? n1 : n2;

@@ -198,7 +198,8 @@ def test_compress_kernel_family_dispatch():
     K = {"fold": 0, "fwht2p": 1, "fft2p": 2, "fwht1p": 3}
     assert _device.compress_kernel("fwht", 3, 12, 8192, 8192, 8192) == K["fwht1p"]   # cfg5 b = 2^12
     assert _device.compress_kernel("fwht", 3, 12, 1024, 1024, 1024) == K["fwht1p"]   # cfg1
-    assert _device.compress_kernel("fwht", 9, 12, 8192, 8192, 8192) == K["fwht2p"]   # d > 7: TMEM budget
+    assert _device.compress_kernel("fwht", 9, 12, 8192, 8192, 8192) == K["fwht1p"]   # d > 7: repetition groups
+    assert _device.compress_kernel("fwht", 63, 12, 8192, 8192, 8192) == K["fwht1p"]
     assert _device.compress_kernel("fwht", 3, 12, 16384, 16384, 16384) == K["fwht2p"]  # columns exceed smem
     assert _device.compress_kernel("fwht", 5, 16, 16384, 16384, 16384) == K["fwht2p"]  # cfg3
     assert _device.compress_kernel("fft", 5, 14, 4096, 4096, 4096) == K["fft2p"]     # cfg2
