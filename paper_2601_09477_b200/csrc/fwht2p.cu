@@ -830,21 +830,25 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   const int64_t total = (int64_t)p.U * (G1 + G2);
   // Scheduling (thread 0) runs one item ahead: the ticket after next is claimed
   // while the current item computes, and every warp prefetches the CSR heads of
-  // the next pass-1 item.  Dependencies (thread 32): right before the closing
+  // the next pass-1 item.  Dependencies (thread 0): right before the closing
   // barrier [B] of item i it issues RELAXED loads of the counters that item i+1
   // depends on (P1(u): every P2 of unit u - nslot, whose Y slot it reuses; P2(u):
   // every P1 of unit u, and the slice's accumulator counter, i.e. the previous
-  // k-tile's P2 of the same accumulator rows).  After [B] its fence.acq_rel both
-  // releases item i (the completion adds that follow) and turns those loads into
-  // acquires (PTX acquire pattern: relaxed read, then fence); a counter not yet
-  // complete is polled there with ld.acquire.  Barrier [A] then extends the order
-  // to the whole CTA, so every Y / accumulator read of item i+1 happens after its
-  // producers' writes.  Every dependency was dispensed before the item that waits
-  // on it, so waiting cannot deadlock.  Scheduler state lives in shared memory (as
+  // k-tile's P2 of the same accumulator rows).  After [B] a fence.acquire turns
+  // those loads into acquires (PTX acquire pattern: relaxed read, then fence; it
+  // does not wait for outstanding stores); a counter not yet complete is polled
+  // with ld.acquire.  Barrier [A] then extends the order to the CTA, so every Y /
+  // accumulator read of item i+1 happens after its producers' writes.  Item i is
+  // published by thread 32 after [B] (fence.release, then the completion adds):
+  // the release waits for the item's Y / accumulator stores to drain, so warp 1
+  // joins [A] through a barrier of its own with warp 0 and the other six warps
+  // start item i+1 meanwhile.  Every dependency was dispensed before the item that
+  // waits on it and a publish never waits for anything but its own stores, so
+  // waiting cannot deadlock.  Scheduler state lives in shared memory (as
   // registers it would cost every thread ~14 of its 128).
   __shared__ int64_t sh_nxt;
   __shared__ Item sh_itn;
-  __shared__ int sh_ver[2];  // highest unit whose completion thread 32 acquired: done1 (P2), done2 (P1)
+  __shared__ int sh_ver[2];  // highest unit whose completion thread 0 acquired: done1 (P2), done2 (P1)
   __shared__ int s_acc_ok;   // the next P2 item's accumulator counter was acquired complete
   int64_t &nxt = sh_nxt;
   Item &itn = sh_itn;
@@ -889,16 +893,14 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     nxt = atomicAdd(ticket, 1);
     itn = decode_item(p, cur, log2g);
     sh_ver[0] = sh_ver[1] = -1;
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (tid == 32) {  // the first item's dependencies (usually none)
-    Deps D;
+    Deps D;  // the first item's dependencies (usually none)
     deps_of(itn, D);
     deps_settle(D);
     s_acc_ok = 0;
   }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   const uint32_t tmem = s_tmem;
   PullHead hd_next, hd_next1;  // both operands' CSR heads of the next pass-1 item
   bool hd_valid = false;
@@ -924,7 +926,15 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     }
     tc_fence_before();
     PROF_MARK(0);
-    __syncthreads();  // [A]
+    // [A]: the item descriptor (thread 0, after acquiring the item's dependencies) reaches the
+    // CTA.  Warp 1 publishes the previous item (a release fence that waits for that item's
+    // stores to drain) and joins through its own barrier, so the other warps start at once.
+    if (warp == 1) {
+      asm volatile("bar.sync 2, 64;" ::: "memory");
+    } else {
+      if (warp == 0) asm volatile("bar.arrive 2, 64;" ::: "memory");
+      asm volatile("bar.sync 1, 224;" ::: "memory");
+    }
     PROF_MARK(1);
     tc_fence_after();
     const int go = s_item[0];
@@ -953,9 +963,9 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
       else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, acc_ok, S);
     }
-    // thread 32: relaxed probe of the next item's dependency counters (acquired by the fence below)
+    // thread 0: relaxed probe of the next item's dependency counters (acquired by the fence below)
     Deps D;
-    if (tid == 32) {
+    if (tid == 0) {
       const Item nx = itn;
       deps_of(nx, D);
 #pragma unroll
@@ -968,13 +978,18 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     PROF_MARK(10);
     tc_fence_after();
     if (tid == 32) {
-      // release this item's writes (covered through [B]) and acquire the probed counters
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      // release this item's writes (covered through [B]), then publish it
+      asm volatile("fence.release.gpu;" ::: "memory");
       if (is_p1) red_add(done1 + u, 1);
       else {
         red_add(acc_cnt + (t * p.F + asl) * p.nblk + idx, 1);
         red_add(done2 + u, 1);
       }
+    }
+    if (tid == 0) {
+      // acquire the probed counters (PTX acquire pattern: relaxed reads, then an acquire fence;
+      // no wait for outstanding stores), poll one that is not yet complete
+      asm volatile("fence.acquire.gpu;" ::: "memory");
       deps_settle(D);
     }
   }
