@@ -510,15 +510,17 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
   int *acc_cnt = done2 + p.U;
   const int64_t total = (int64_t)p.U * (p.G1 + p.G2);
   // Thread 0 schedules one item ahead (the ticket after next is claimed while the
-  // current item computes).  Dependencies, as fwht2p: thread 32 issues RELAXED loads
-  // of the next item's counters right before [B]; after [B] its fence.acq_rel releases
-  // this item (the completion adds) and acquires those counters; an incomplete
-  // must-precede counter is polled there with ld.acquire; [A] orders the whole CTA.
+  // current item computes).  Dependencies, as fwht2p: thread 0 issues RELAXED loads
+  // of the next item's counters right before [B]; after [B] its fence.acquire
+  // acquires them (an incomplete must-precede counter is polled with ld.acquire) and
+  // [A] orders the CTA.  Thread 32 publishes the item after [B] (fence.release, then
+  // the completion adds); warp 1 joins [A] through its own barrier with warp 0, so the
+  // release's wait for the item's stores does not hold the other warps.
   // The accumulator counter (previous k-tile's P2 of the same rows) is only recorded:
   // if incomplete, the P2 item waits for it per warp at its end (acc_ready).
   __shared__ int64_t sh_nxt;
   __shared__ Item sh_itn;
-  __shared__ int sh_ver[2];  // highest unit thread 32 acquired: done1 (P2 items), done2 (P1 slot reuse)
+  __shared__ int sh_ver[2];  // highest unit thread 0 acquired: done1 (P2 items), done2 (P1 slot reuse)
   __shared__ int s_acc_ok;
   int64_t &nxt = sh_nxt;
   Item &itn = sh_itn;
@@ -559,16 +561,14 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
     nxt = atomicAdd(ticket, 1);
     itn = decode_item(p, cur);
     sh_ver[0] = sh_ver[1] = -1;
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (tid == 32) {  // the first item's dependencies
-    Deps D;
+    Deps D;  // the first item's dependencies
     deps_of(itn, D);
     deps_settle(D);
     s_acc_ok = 0;
   }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   const uint32_t tmem = s_tmem;
   while (true) {
     if (tid == 0) {
@@ -587,7 +587,12 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
       itn = decode_item(p, nxt);
     }
     tc_fence_before();
-    __syncthreads();  // [A]
+    if (warp == 1) {  // [A] (warp 1 may still be publishing the previous item)
+      asm volatile("bar.sync 2, 64;" ::: "memory");
+    } else {
+      if (warp == 0) asm volatile("bar.arrive 2, 64;" ::: "memory");
+      asm volatile("bar.sync 1, 224;" ::: "memory");
+    }
     tc_fence_after();
     const int go = s_item[0];
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
@@ -598,8 +603,8 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
     int *acc_flag = acc_cnt + (t * p.NPU + pu) * p.G2 + idx;
     if (is_p1) p1_item<S1, FOLD>(p, kappa, t, pu, slot, idx, S);
     else p2_item(p, kappa, t, pu, slot, idx, tmem, acc_flag, acc_ok, S);
-    Deps D;  // thread 32: relaxed probe of the next item's counters (acquired by the fence below)
-    if (tid == 32) {
+    Deps D;  // thread 0: relaxed probe of the next item's counters (acquired by the fence below)
+    if (tid == 0) {
       const Item nx = itn;
       deps_of(nx, D);
 #pragma unroll
@@ -609,13 +614,16 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
     tc_fence_before();
     __syncthreads();  // [B]
     tc_fence_after();
-    if (tid == 32) {  // release this item (covered through [B]); acquire the probed counters
-      fence_acq_rel();
+    if (tid == 32) {  // release this item (covered through [B]), then publish it
+      asm volatile("fence.release.gpu;" ::: "memory");
       if (is_p1) red_add(done1 + u, 1);
       else {
         red_add(acc_flag, 1);
         red_add(done2 + u, 1);
       }
+    }
+    if (tid == 0) {  // acquire the probed counters (relaxed reads, then an acquire fence)
+      asm volatile("fence.acquire.gpu;" ::: "memory");
       deps_settle(D);
     }
   }
