@@ -18,8 +18,7 @@ from __future__ import annotations
 import numpy as np
 
 from .errors import InvalidParameterError
-from .hashing import SketchHashes
-from .sketch import ProductSketch, SketchParams, effective_threads
+from .sketch import ProductSketch, SketchParams, _drawn, effective_threads
 
 
 K_TILE = 32  # inner indices per k-tile of the compress kernels
@@ -65,13 +64,13 @@ def compress_sharded(a_slab, b_slab, params: SketchParams, n_rows: int | None = 
     n1 = a_slab.shape[0] if a_layout == _device.KMINOR else a_slab.shape[1]
     if kl != b_slab.shape[0]:
         raise InvalidParameterError(f"inner slabs must match, got {kl} and {b_slab.shape[0]}")
-    hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
+    hashes, words = _drawn(int(params.seed), params.d, params.b)
     if not getattr(a_slab, "is_cuda", False) and not getattr(b_slab, "is_cuda", False):
         # host slabs: streamed upload overlapped with the compress kernel
-        acc = _device.compress_host(_device.host_f64(a_slab), _device.host_f64(b_slab), hashes.packed_words(),
+        acc = _device.compress_host(_device.host_f64(a_slab), _device.host_f64(b_slab), words,
                                     params.d, params.log2b, params.transform, a_layout, _device.require_cuda())
     else:
-        acc = _device.compress_accumulate(a_slab, b_slab, hashes.packed_words(), params.d, params.log2b,
+        acc = _device.compress_accumulate(a_slab, b_slab, words, params.d, params.log2b,
                                           params.transform, 0, kl, a_layout=a_layout)
     reduce_accumulator(acc, group=group, all_reduce=all_reduce)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)

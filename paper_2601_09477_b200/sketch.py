@@ -20,6 +20,7 @@ Reference behaviour kept on purpose:
 
 from __future__ import annotations
 
+import functools
 import math
 import struct
 from dataclasses import dataclass, field
@@ -198,6 +199,22 @@ def _check_2d(m, what: str):
     return shp
 
 
+@functools.lru_cache(maxsize=256)
+def _drawn(seed: int, d: int, b: int):
+    """The sketch's hash functions and their packed words for (seed, d, b).
+
+    The draw is a pure function of the seed (``default_rng(seed)``, the reference's
+    order, hashing.py:78-132), and ``SketchHashes`` is immutable, so repeated
+    compress calls with the same parameters reuse it: the numpy draw costs ~170 us of
+    host time per call, which small sketches (cfg1: ~0.3 ms of device work) would
+    otherwise spend with the GPU idle.
+    """
+    hashes = SketchHashes.draw(np.random.default_rng(seed), d, b)
+    words = hashes.packed_words()
+    words.setflags(write=False)
+    return hashes, words
+
+
 def _run(a, b, params: SketchParams, threads, a_layout: int, b_layout: int = 0) -> ProductSketch:
     """Steps 1-4 on device-resident operands (the reference's _run_kernel, sketch.py:238-260).
 
@@ -211,9 +228,9 @@ def _run(a, b, params: SketchParams, threads, a_layout: int, b_layout: int = 0) 
     if m_a != b.shape[0]:
         raise InvalidParameterError(f"inner dimensions must match, got {m_a} and {b.shape[0]}")
     effective_threads(threads)
-    hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
+    hashes, words = _drawn(int(params.seed), params.d, params.b)
     _check_depth(params)
-    acc = _device.compress_accumulate(a, b, hashes.packed_words(), params.d, params.log2b, params.transform, 0, m_a,
+    acc = _device.compress_accumulate(a, b, words, params.d, params.log2b, params.transform, 0, m_a,
                                       a_layout=a_layout, b_layout=b_layout)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)
     n_rows = a.shape[0] if a_layout == _device.KMINOR else a.shape[1]
@@ -238,9 +255,9 @@ def _run_host(a, b, params: SketchParams, threads, a_layout: int, dev) -> Produc
     a = _device.host_f64(a)
     b = _device.host_f64(b)
     effective_threads(threads)
-    hashes = SketchHashes.draw(np.random.default_rng(params.seed), params.d, params.b)
+    hashes, words = _drawn(int(params.seed), params.d, params.b)
     _check_depth(params)
-    acc = _device.compress_host(a, b, hashes.packed_words(), params.d, params.log2b, params.transform, a_layout, dev)
+    acc = _device.compress_host(a, b, words, params.d, params.log2b, params.transform, a_layout, dev)
     polys = _device.finalize(acc, params.d, params.log2b, params.transform)
     n_rows = a.shape[0] if a_layout == _device.KMINOR else a.shape[1]
     return ProductSketch(polys=polys, hashes=hashes, params=params, n_rows=n_rows, n_cols=b.shape[1])
@@ -342,7 +359,7 @@ def compress_seeds(a, b, params: SketchParams, seeds, threads: int | None = None
     out = []
     for g0 in range(0, len(per), group):
         ps = per[g0:g0 + group]
-        hs = [SketchHashes.draw(np.random.default_rng(p.seed), d, p.b) for p in ps]
+        hs = [_drawn(int(p.seed), d, p.b)[0] for p in ps]
         stacked = SketchHashes(h1=sum((h.h1 for h in hs), ()), h2=sum((h.h2 for h in hs), ()),
                                s1=sum((h.s1 for h in hs), ()), s2=sum((h.s2 for h in hs), ()))
         words = stacked.packed_words()

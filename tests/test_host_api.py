@@ -75,6 +75,18 @@ class TestHashing:
         with pytest.raises(InvalidParameterError):
             HashPair(a=0, c=0, shift=20)
 
+    def test_cached_draw_equals_reference_draw(self, draws_golden):
+        # compress reuses the draw per (seed, d, b) (sketch._drawn): same words as a fresh
+        # default_rng(seed) draw, and the shared words cannot be modified in place
+        from paper_2601_09477_b200.sketch import _drawn
+
+        for e in draws_golden[:40]:
+            for _ in range(2):
+                h, w = _drawn(int(e["seed"]), e["d"], e["b"])
+                assert [str(int(x)) for x in w] == e["words"]
+                assert h == SketchHashes.draw(np.random.default_rng(int(e["seed"])), e["d"], e["b"])
+                assert not w.flags.writeable
+
     def test_json_round_trip(self):
         g = SketchHashes.draw(np.random.default_rng(3), 5, 256)
         assert SketchHashes.from_json_obj(json.loads(json.dumps(g.to_json_obj()))) == g
