@@ -116,24 +116,28 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference arm
 def _oracle_sample(w, k_slice: int, row_slice: int, threads: int):
-    """Time the CPU oracle (reference algorithm, bit-exact port) on a bounded sample of w."""
+    """Time the CPU oracle (reference algorithm, bit-exact port) on a bounded sample of w:
+    the A^T copy and compress of a k-slice, the inverse, the estimates of a row slice and
+    their threshold, each scaled to the full product (the same steps _oracle_full times)."""
     from oracle import sketch_oracle as O
 
     words = O.draw_words(w.sketch_seed, w.d, w.b)
-    at = np.ascontiguousarray(w.a[:, :k_slice].T)  # rows k of A^T for the k-slice (as the reference copies A.T)
-    bm = np.ascontiguousarray(w.bmat[:k_slice])
     t0 = time.perf_counter()
-    acc = O.accumulate_fwht(at, bm, b=w.b, d=w.d, words=words, k0=0, k1=k_slice, threads=threads)
+    at = np.ascontiguousarray(w.a[:, :k_slice].T)  # rows k of A^T for the k-slice (as the reference copies A.T)
+    acc = O.accumulate_fwht(at, w.bmat[:k_slice], b=w.b, d=w.d, words=words, k0=0, k1=k_slice, threads=threads)
     tk = time.perf_counter() - t0
+    del at
     t0 = time.perf_counter()
     polys = O.fwht_inverse_scaled(acc)
     tf = time.perf_counter() - t0
     t0 = time.perf_counter()
-    O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, r0=0, r1=row_slice,
-                 want_est=True, thr=w.threshold, strict=True, threads=threads)
+    est, _, _ = O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, r0=0,
+                             r1=row_slice, want_est=True, threads=threads)
+    hh = np.argwhere(np.abs(est) > w.threshold)  # the reference's threshold (experiments.py:136-168)
     tr = time.perf_counter() - t0
     full_ms = (tk * w.n / k_slice + tf + tr * w.n / row_slice) * 1e3
-    return full_ms, {"k_slice": k_slice, "row_slice": row_slice, "t_k_s": tk, "t_rows_s": tr, "t_inv_s": tf}
+    return full_ms, {"k_slice": k_slice, "row_slice": row_slice, "t_k_s": tk, "t_rows_s": tr, "t_inv_s": tf,
+                     "heavy_hitters_in_rows": int(hh.shape[0])}
 
 
 def _cpu_instance(cfg: str):
@@ -154,7 +158,8 @@ def _calibrate(w, threads: int, budget_s: float):
 def _oracle_full(w, threads: int):
     """One full sketched product on the CPU oracle (the reference's algorithm, bit-exact
     port): A^T copy (sketch.py:305), compress over every inner index, inverse, all n^2
-    estimates (sketch.py:375-399), threshold and the row-major pair list."""
+    estimates (sketch.py:375-399), then the reference's threshold — numpy over the
+    estimate matrix, as experiments.py:136-168 does — giving the row-major pair list."""
     from oracle import sketch_oracle as O
 
     words = O.draw_words(w.sketch_seed, w.d, w.b)
@@ -165,11 +170,13 @@ def _oracle_full(w, threads: int):
     t1 = time.perf_counter()
     polys = O.fwht_inverse_scaled(acc)
     t2 = time.perf_counter()
-    _, cnt, _ = O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, want_est=True,
-                             thr=w.threshold, strict=True, want_hh=True, threads=threads)
+    est, _, _ = O.decompress(polys, words, b=w.b, d=w.d, transform=w.transform, n1=w.n, n2=w.n, want_est=True,
+                             threads=threads)
     t3 = time.perf_counter()
-    return (t3 - t0) * 1e3, {"compress_s": t1 - t0, "inverse_s": t2 - t1, "decompress_threshold_s": t3 - t2,
-                             "heavy_hitters": int(cnt)}
+    hh = np.argwhere(np.abs(est) > w.threshold)
+    t4 = time.perf_counter()
+    return (t4 - t0) * 1e3, {"compress_s": t1 - t0, "inverse_s": t2 - t1, "decompress_s": t3 - t2,
+                             "threshold_s": t4 - t3, "heavy_hitters": int(hh.shape[0])}
 
 
 def _stock_reference(w):
@@ -218,6 +225,7 @@ def run_reference(args) -> None:
     info = None
     for step in range(args.warmup + args.steps):
         ms, info = _oracle_full(w, threads)
+        print(f"reference step {step}: {ms:.0f} ms {info}", file=sys.stderr, flush=True)
         if step >= args.warmup:
             times.append(ms)
     value = float(np.median(times))
