@@ -86,6 +86,7 @@ int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int
 #define SMM_KERNEL_FWHT2P 1 /* two-pass FWHT, 2^8 <= b <= 2^20               */
 #define SMM_KERNEL_FFT2P 2  /* two-pass FFT                                   */
 #define SMM_KERNEL_FWHT1P 3 /* one-pass FWHT, b = 2^12, n1 + n2 <= 16384 (launches of <= 7 repetitions) */
+#define SMM_KERNEL_FFT1P 4  /* one-pass FFT, b = 2^12, n1 + n2 <= 16384 (launches of <= 7 repetitions) */
 int smm_compress_kernel(int variant, int d, int log2b, int64_t n1, int64_t n2, int64_t k0, int64_t k1,
                         int *kernel);
 

@@ -10,6 +10,11 @@ int64_t fwht_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K, int 
 int64_t fft_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K, int Gmax);
 bool fwht2p_supported(int log2b, int64_t n1, int64_t n2);
 bool fwht1p_supported(int log2b, int d, int64_t n1, int64_t n2, int64_t K);
+bool fft1p_supported(int log2b, int d, int64_t n1, int64_t n2, int64_t K);
+int64_t fft1p_workspace(int d, int64_t n1, int64_t n2, int64_t K);
+int fft1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const double *xb, int64_t ldb, int64_t n1,
+                     int64_t n2, int64_t k0, int64_t k1, double *acc, bool acc_add, char *ws, int64_t ws_bytes,
+                     cudaStream_t s);
 int64_t fwht1p_workspace(int d, int64_t n1, int64_t n2, int64_t K);
 int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool a_kminor, const double *xb,
                       int64_t ldb, bool b_kminor, int64_t n1, int64_t n2, int64_t k0, int64_t k1, double *acc,
@@ -125,7 +130,7 @@ int smm_hash_tables(const uint64_t *words_host, int d, int log2b, int group, int
 // SMM_FLAG_ACCUMULATE: the two-pass kernel continues the k order in acc itself;
 // the other kernels reduce into a workspace accumulator that is then added.
 struct CompressPlan {
-  bool one_pass, two_pass, fft_two_pass, acc_add;
+  bool one_pass, fft_one_pass, two_pass, fft_two_pass, acc_add;
   bool ta, tb;  // transpose A / B slab
   int64_t ta_bytes, tb_bytes, tmp_acc_bytes, kernel_bytes;
 };
@@ -134,8 +139,9 @@ static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int
                                   int blay, bool acc_add) {
   CompressPlan c;
   c.acc_add = acc_add;
-  c.fft_two_pass = variant == SMM_VARIANT_FFT && fft2p_supported(log2b, n1, n2);
-  // one-pass on-chip kernel for b = 2^12 with small operands (fwht1p.cu); k-major operands
+  // one-pass on-chip kernels for b = 2^12 with small operands (fwht1p.cu, fft1p.cu); k-major operands
+  c.fft_one_pass = variant == SMM_VARIANT_FFT && fft1p_supported(log2b, d, n1, n2, K);
+  c.fft_two_pass = !c.fft_one_pass && variant == SMM_VARIANT_FFT && fft2p_supported(log2b, n1, n2);
   c.one_pass = variant == SMM_VARIANT_FWHT && fwht1p_supported(log2b, d, n1, n2, K);
   c.two_pass = !c.one_pass && ((variant == SMM_VARIANT_FWHT && fwht2p_supported(log2b, n1, n2)) || c.fft_two_pass);
   // two-pass kernels read k-minor rows, the others k-major ones; the one-pass kernel could
@@ -147,11 +153,12 @@ static CompressPlan plan_compress(int variant, int d, int log2b, int64_t n1, int
   c.ta_bytes = c.ta ? ((n1 * K * 8 + 255) / 256) * 256 : 0;
   c.tb_bytes = c.tb ? ((n2 * K * 8 + 255) / 256) * 256 : 0;
   if (c.one_pass) c.kernel_bytes = fwht1p_workspace(d, n1, n2, K);
+  else if (c.fft_one_pass) c.kernel_bytes = fft1p_workspace(d, n1, n2, K);
   else if (c.fft_two_pass) c.kernel_bytes = fft2p_workspace(d, log2b, n1, n2, K);
   else if (c.two_pass) c.kernel_bytes = fwht2p_workspace(d, log2b, n1, n2, K);
   else if (variant == SMM_VARIANT_FWHT) c.kernel_bytes = fwht_workspace(d, log2b, n1, n2, K, num_sms());
   else c.kernel_bytes = fft_workspace(d, log2b, n1, n2, K, num_sms());
-  c.tmp_acc_bytes = (acc_add && !c.two_pass && !c.one_pass) ? ((acc_bytes(variant, d, log2b) + 255) / 256) * 256 : 0;
+  c.tmp_acc_bytes = (acc_add && !c.two_pass && !c.one_pass && !c.fft_one_pass) ? ((acc_bytes(variant, d, log2b) + 255) / 256) * 256 : 0;
   return c;
 }
 
@@ -179,8 +186,11 @@ int smm_compress_kernel(int variant, int d, int log2b, int64_t n1, int64_t n2, i
   variant &= ~SMM_FLAG_ACCUMULATE;
   const int dg = d < SMM_MAX_DEPTH ? d : SMM_MAX_DEPTH;
   CompressPlan c = plan_compress(variant, dg, log2b, n1, n2, k1 - k0, SMM_LAYOUT_KMAJOR, SMM_LAYOUT_KMAJOR, false);
-  *kernel = c.one_pass ? SMM_KERNEL_FWHT1P : c.fft_two_pass ? SMM_KERNEL_FFT2P : c.two_pass ? SMM_KERNEL_FWHT2P
-                                                                                            : SMM_KERNEL_FOLD;
+  *kernel = c.one_pass       ? SMM_KERNEL_FWHT1P
+            : c.fft_one_pass ? SMM_KERNEL_FFT1P
+            : c.fft_two_pass ? SMM_KERNEL_FFT2P
+            : c.two_pass     ? SMM_KERNEL_FWHT2P
+                             : SMM_KERNEL_FOLD;
   return SMM_OK;
 }
 
@@ -255,6 +265,8 @@ int smm_compress_accumulate_ex(int variant, const double *a, int64_t lda, int a_
     if (c.one_pass)
       rc = fwht1p_accumulate(h, xa, la, false, xb, lb, false, n1, n2, kk0, kk1, (double *)accg, acc_add, kws, kb,
                              s);  // k-major views (transposed above when needed)
+    else if (c.fft_one_pass)
+      rc = fft1p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)accg, acc_add, kws, kb, s);
     else if (c.fft_two_pass)
       rc = fft2p_accumulate(h, xa, la, xb, lb, n1, n2, kk0, kk1, (double *)accg, acc_add, kws, kb, s);
     else if (c.two_pass)

@@ -312,6 +312,32 @@ def test_public_api_host_operands_bitwise_equal_to_device_operands():
     assert np.array_equal(dev_sk.polys, np_sk.polys)
 
 
+@pytest.mark.parametrize("d", [3, 9])
+def test_one_pass_fft_host_streamed_bitwise_and_oracle(d):
+    """fft1p (b = 2^12, rectangular, non-integer data): host operands streamed in k-slabs
+    (SMM_FLAG_ACCUMULATE) give the device call's bits; polys and estimates against the CPU
+    oracle within the north star's 1e-10 * ||C||_F; d = 9 runs as two launches."""
+    from oracle import sketch_oracle as O
+    from paper_2601_09477_b200 import _device
+
+    rng = np.random.default_rng(17 + d)
+    n1, m, n2 = 700, 1000, 900
+    a = rng.standard_normal((n1, m))
+    bm = rng.standard_normal((m, n2))
+    p = P.SketchParams(n=m, b=1 << 12, d=d, transform="fft", seed=29)
+    assert _device.compress_kernel("fft", d, 12, n1, n2, m) == 4  # SMM_KERNEL_FFT1P
+    dev = P.compress_rect(torch.as_tensor(a, device="cuda"), torch.as_tensor(bm, device="cuda"), p)
+    host = P.compress_rect(torch.as_tensor(a).pin_memory(), torch.as_tensor(bm), p)
+    assert np.array_equal(dev.polys, host.polys)
+    ref = O.compress(a, bm, b=p.b, d=d, transform="fft", seed=p.seed, threads=4)
+    cf = np.linalg.norm(a @ bm)
+    assert np.max(np.abs(dev.polys - ref)) <= 1e-10 * cf
+    est = P.decompress_all(dev)
+    est_ref, _, _ = O.decompress(ref, O.draw_words(p.seed, d, p.b), b=p.b, d=d, transform="fft", n1=n1, n2=n2,
+                                 want_est=True, threads=4)
+    assert np.max(np.abs(est - est_ref)) <= 1e-10 * cf
+
+
 def test_extract_to_host_matches_device():
     w = W.make("cfg1", xp=torch, device="cuda")
     p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)

@@ -207,7 +207,7 @@ def test_compress_kernel_family_dispatch():
     seeds only within one family, so every sketch keeps its single-call bits)."""
     from paper_2601_09477_b200 import _device
 
-    K = {"fold": 0, "fwht2p": 1, "fft2p": 2, "fwht1p": 3}
+    K = {"fold": 0, "fwht2p": 1, "fft2p": 2, "fwht1p": 3, "fft1p": 4}
     assert _device.compress_kernel("fwht", 3, 12, 8192, 8192, 8192) == K["fwht1p"]   # cfg5 b = 2^12
     assert _device.compress_kernel("fwht", 3, 12, 1024, 1024, 1024) == K["fwht1p"]   # cfg1
     assert _device.compress_kernel("fwht", 9, 12, 8192, 8192, 8192) == K["fwht1p"]   # d > 7: repetition groups
@@ -215,4 +215,7 @@ def test_compress_kernel_family_dispatch():
     assert _device.compress_kernel("fwht", 3, 12, 16384, 16384, 16384) == K["fwht2p"]  # columns exceed smem
     assert _device.compress_kernel("fwht", 5, 16, 16384, 16384, 16384) == K["fwht2p"]  # cfg3
     assert _device.compress_kernel("fft", 5, 14, 4096, 4096, 4096) == K["fft2p"]     # cfg2
+    assert _device.compress_kernel("fft", 5, 12, 8192, 8192, 8192) == K["fft1p"]     # cfg5 b = 2^12 FFT
+    assert _device.compress_kernel("fft", 9, 12, 8192, 8192, 8192) == K["fft1p"]
+    assert _device.compress_kernel("fft", 3, 12, 16384, 16384, 16384) == K["fft2p"]  # columns exceed smem
     assert _device.compress_kernel("fwht", 3, 6, 100, 100, 100) == K["fold"]         # b < 2^8
