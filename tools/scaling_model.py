@@ -5,7 +5,7 @@ runs: compress of its k-slab (B-slab transpose, CSR plan, fwht2p), the inverse, 
 the extraction + threshold of its n/N output rows.  This times exactly that work for
 the slowest rank on cuda:0 (inputs resident, CUDA events, median of reps); the one
 collective (a d x b float64 allreduce) is not run here (one GPU per call) and is
-listed by size.  Output: one JSON line per N, and profiles/r01_scaling_model.json.
+listed by size.  Output: one JSON line per N, and profiles/<SMM_ROUND>_scaling_model_<cfg>.json.
 
     python tools/scaling_model.py [cfg3|cfg4]
 """
@@ -66,6 +66,6 @@ base = rows[0]["rank_ms"]
 for r in rows:
     r["speedup_vs_1"] = base / r["rank_ms"]
     r["efficiency"] = base / (r["rank_ms"] * r["n_gpus"])
-out = ROOT / "profiles" / f"r01_scaling_model_{cfg}.json"
+out = ROOT / "profiles" / f"{__import__('os').environ.get('SMM_ROUND', 'r02')}_scaling_model_{cfg}.json"
 out.write_text(json.dumps(rows, indent=1))
 print(json.dumps(rows))
