@@ -338,6 +338,30 @@ def test_one_pass_fft_host_streamed_bitwise_and_oracle(d):
     assert np.max(np.abs(est - est_ref)) <= 1e-10 * cf
 
 
+@pytest.mark.parametrize("transform", ["fwht", "fft"])
+@pytest.mark.parametrize("n1,m,n2,d", [(1, 37, 5000, 3), (3000, 33, 2, 5), (8191, 41, 8192, 1), (500, 1, 700, 7),
+                                       (16383, 9, 1, 3)])
+def test_one_pass_edge_shapes_against_oracle(transform, n1, m, n2, d):
+    """fwht1p / fft1p (b = 2^12) on ragged shapes: one-row and one-column operands, an
+    inner range that is not a multiple of the 8-wide tiles, a single inner index, and
+    n1 + n2 at the 16384 staging limit; against the CPU oracle (bit-exact for integer
+    data, which these operands are)."""
+    from oracle import sketch_oracle as O
+    from paper_2601_09477_b200 import _device
+
+    rng = np.random.default_rng(n1 * 7 + m)
+    a = rng.integers(-3, 4, size=(n1, m)).astype(np.float64)
+    bm = rng.integers(-3, 4, size=(m, n2)).astype(np.float64)
+    p = P.SketchParams(n=m, b=1 << 12, d=d, transform=transform, seed=41)
+    assert _device.compress_kernel(transform, d, 12, n1, n2, m) == (3 if transform == "fwht" else 4)
+    sk = P.compress_rect(torch.as_tensor(a, device="cuda"), torch.as_tensor(bm, device="cuda"), p)
+    ref = O.compress(a, bm, b=p.b, d=d, transform=transform, seed=p.seed, threads=4)
+    if transform == "fwht":
+        assert np.array_equal(sk.polys, ref)
+    else:
+        assert np.max(np.abs(sk.polys - ref)) <= 1e-10 * max(1.0, np.linalg.norm(a @ bm))
+
+
 def test_extract_to_host_matches_device():
     w = W.make("cfg1", xp=torch, device="cuda")
     p = P.SketchParams(n=w.n, b=w.b, d=w.d, transform=w.transform, seed=w.sketch_seed)
