@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(CT, 1) fft1p_kernel(Args p) {
   };
   // rev3(n): base-8 digit reversal of n < 512; position 8n + r' holds frequency 512 r' + rev3(n)
   const int rev_n = ((tid & 7) << 6) | (((tid >> 3) & 7) << 3) | (tid >> 6);
+  // the thread's slot r of the exchange area: zidx(tid + 512 r) = zidx(tid) + 576 r
+  const int zb = 2 * zidx(tid);
   int64_t tile = blockIdx.x;
   if (tile < p.ntiles) {
     column_copy(p, 0, tile * p.W, colA);
@@ -237,14 +239,14 @@ __global__ void __launch_bounds__(CT, 1) fft1p_kernel(Args p) {
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
               run = ((w[r] & W_FIRST) ? 0.0 : run) + x[r];
-              if (w[r] & W_LAST) zd[2 * zidx(tid + 512 * (int)((w[r] >> 17) & 7u)) + op] = run;
+              if (w[r] & W_LAST) zd[zb + op + 1152 * (int)((w[r] >> 17) & 7u)] = run;
             }
           }
         }
         cplx v[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const int zi = 2 * zidx(tid + 512 * r);
+          const int zi = zb + 1152 * r;
           v[r].re = ((mask[0] >> r) & 1u) ? zd[zi] : 0.0;
           v[r].im = ((mask[1] >> r) & 1u) ? zd[zi + 1] : 0.0;
         }
