@@ -80,6 +80,7 @@ struct Args {
   const uint32_t *bmask;  // [d][2][CT]: slots of each thread's 8 that have an entry
   cplx *part;            // [ntiles][d][HALF + 1]
   int vec16;             // per operand: 16-byte async copies allowed
+  int bulk;              // both columns are staged with TMA bulk copies (contiguous, 16-byte aligned)
 };
 
 __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
@@ -156,14 +157,33 @@ __global__ void __launch_bounds__(CT, 1) fft1p_kernel(Args p) {
   __shared__ uint32_t s_tmem;
   __shared__ cplx s_t0[64], s_t1[64];  // w_4096^e = s_t1[e >> 6] * s_t0[e & 63]
   __shared__ cplx s_acc_half[MAXD];    // the tile's u = 2048 accumulators (thread 0)
+  __shared__ __align__(8) uint64_t s_colbar;  // bulk column copies landed
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   cplx *Z = (cplx *)sm;                                     // exchange area, ZS padded slots
   double *zd = sm;                                          // the same, as doubles
   double *colA = sm + 2 * ZS;                               // staged columns, each followed by a zero
   double *colB = colA + ((p.n[0] + 2) & ~1);
-  if (tid == 0) colA[p.n[0]] = 0.0;
+  if (tid == 0) {
+    colA[p.n[0]] = 0.0;
+    mbar_init(&s_colbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (tid == 1) colB[p.n[1]] = 0.0;
+  uint32_t colpar = 0;  // phase parity of the next bulk copy pair
+  // the inner index k's columns: one elected thread issues both bulk copies, or every thread
+  // its cp.async share
+  auto stage = [&](int64_t kk) {
+    if (p.bulk) {
+      if (tid == 0)
+        bulk_copy2_g2s(colA, p.X[0] + kk * p.ks[0], (uint32_t)p.n[0] * 8u, colB, p.X[1] + kk * p.ks[1],
+                       (uint32_t)p.n[1] * 8u, &s_colbar);
+    } else {
+      column_copy(p, 0, kk, colA);
+      column_copy(p, 1, kk, colB);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
   const uint32_t col_s[2] = {(uint32_t)__cvta_generic_to_shared(colA), (uint32_t)__cvta_generic_to_shared(colB)};
   if (tid < 64) {
     double sn, cs;
@@ -196,16 +216,17 @@ __global__ void __launch_bounds__(CT, 1) fft1p_kernel(Args p) {
   // the thread's slot r of the exchange area: zidx(tid + 512 r) = zidx(tid) + 576 r
   const int zb = 2 * zidx(tid);
   int64_t tile = blockIdx.x;
-  if (tile < p.ntiles) {
-    column_copy(p, 0, tile * p.W, colA);
-    column_copy(p, 1, tile * p.W, colB);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  if (tile < p.ntiles) stage(tile * p.W);  // (the barrier above ordered the mbarrier's initialisation)
   for (; tile < p.ntiles; tile += gridDim.x) {
     const int64_t k_lo = tile * p.W;
     const int64_t k_hi = k_lo + p.W < p.K ? k_lo + p.W : p.K;
     for (int64_t k = k_lo; k < k_hi; ++k) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (p.bulk) {
+        mbar_wait(&s_colbar, colpar);
+        colpar ^= 1u;
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
       __syncthreads();  // the columns are visible; the exchange area is free
       for (int t = 0; t < d; ++t) {
         // ---- signed scatter: real part from A's entries, imaginary part from B's, into this
@@ -258,11 +279,7 @@ __global__ void __launch_bounds__(CT, 1) fft1p_kernel(Args p) {
             const int64_t tn = tile + gridDim.x;
             kn = tn < p.ntiles ? tn * p.W : -1;
           }
-          if (kn >= 0) {
-            column_copy(p, 0, kn, colA);
-            column_copy(p, 1, kn, colB);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-          }
+          if (kn >= 0) stage(kn);
         }
         // ---- 4096-point DFT: decimation in frequency, radix 8, four stages in place
         cplx w[8];
@@ -596,6 +613,8 @@ int fft1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, const
   p.vec16 = 0;
   if (p.ks[0] % 2 == 0 && n1 % 2 == 0 && (uintptr_t)p.X[0] % 16 == 0) p.vec16 |= 1;
   if (p.ks[1] % 2 == 0 && n2 % 2 == 0 && (uintptr_t)p.X[1] % 16 == 0) p.vec16 |= 2;
+  static const bool no_bulk = getenv("SMM_NO_BULK_COLUMNS") != nullptr;
+  p.bulk = (!no_bulk && p.vec16 == 3) ? 1 : 0;
   const size_t smem = (size_t)(2 * ZS + ((n1 + 2) & ~1) + n2 + 1) * 8;
   SMM_CUDA_TRY(cudaFuncSetAttribute(fft1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "fft1p smem");

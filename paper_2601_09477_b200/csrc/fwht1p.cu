@@ -69,6 +69,7 @@ struct Args {
   const uint32_t *bmask;  // [d][2][256]: buckets of each thread's 16 that have an entry
   double *part;          // [ntiles][d][B]
   int vec16;             // both operands allow 16-byte async copies
+  int bulk;              // per operand: the column is staged with one TMA bulk copy
 };
 
 // exchange layout: one pad double per 16 (every access pattern below is conflict-free,
@@ -98,9 +99,15 @@ __device__ __forceinline__ void fwht16(double (&v)[16]) {
 // operand (A row-major) is read with 8-byte copies at stride is: 4x the L2 sectors, but
 // the neighbouring inner indices of each sector are the CTA's next columns (L2 hits), and
 // no transposed copy of the operand is needed
-__device__ __forceinline__ void column_copy(const Args &p, int h, int64_t k, double *col, int ht) {
+// A contiguous column with 16-byte alignment is one TMA bulk copy issued by thread 0 of the
+// half and counted on the half's mbarrier (the LSU then carries none of the staging traffic)
+__device__ __forceinline__ void column_copy(const Args &p, int h, int64_t k, double *col, int ht, uint64_t *bar) {
   const double *src = p.X[h] + k * p.ks[h];
   const int n = p.n[h];
+  if (p.bulk & (1 << h)) {
+    if (ht == 0 && n > 0) bulk_copy_g2s(col, src, (uint32_t)n * 8u, bar);
+    return;
+  }
   if (p.is[h] != 1) {
     const int64_t st = p.is[h];
     for (int i = ht; i < n; i += HT) {
@@ -124,6 +131,7 @@ __device__ __forceinline__ void column_copy(const Args &p, int h, int64_t k, dou
 __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
   extern __shared__ __align__(16) double sm[];
   __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t s_colbar[2];  // per half: bulk column copy landed
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int h = tid >> 8;   // 0: operand A, 1: operand B
@@ -132,7 +140,13 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
   double *X = sm + h * XS;  // this half's exchange area (34 KB)
   // staged columns, each followed by one zero double (the padding words' target)
   double *col = sm + 2 * XS + (h ? ((p.n[0] + 2) & ~1) : 0);
-  if (ht == 0) col[p.n[h]] = 0.0;
+  if (ht == 0) {
+    col[p.n[h]] = 0.0;
+    mbar_init(&s_colbar[h], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const bool bulk = (p.bulk >> h) & 1 && p.n[h] > 0;
+  uint32_t colpar = 0;  // phase parity of the next bulk copy
   const uint32_t col_s = (uint32_t)__cvta_generic_to_shared(col);
   double *cells = X + 17 * ht;  // this thread's 16 buckets [16 ht, 16 ht + 16) in the padded layout
   if (warp == 0) {
@@ -151,12 +165,20 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
   bool fa_pending = false;  // half A: B's half has not yet consumed the previous transform
   int64_t tile = blockIdx.x;
   int64_t k = tile * p.W;
-  if (tile < p.ntiles) column_copy(p, h, k, col, ht);
+  if (tile < p.ntiles) {
+    __syncthreads();  // the mbarriers are initialised
+    column_copy(p, h, k, col, ht, &s_colbar[h]);
+  }
   for (; tile < p.ntiles; tile += gridDim.x) {
     const int64_t k_lo = tile * p.W;
     const int64_t k_hi = k_lo + p.W < p.K ? k_lo + p.W : p.K;
     for (k = k_lo; k < k_hi; ++k) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (bulk) {
+        mbar_wait(&s_colbar[h], colpar);
+        colpar ^= 1u;
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
       bar_half(h);  // the column is visible to the whole half; the exchange area is free
       for (int t = 0; t < d; ++t) {
         // ---- signed scatter of column k into this thread's 16 buckets [16 ht, 16 ht + 16):
@@ -201,7 +223,7 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
             const int64_t tn = tile + gridDim.x;
             kn = tn < p.ntiles ? tn * p.W : -1;
           }
-          if (kn >= 0) column_copy(p, h, kn, col, ht);
+          if (kn >= 0) column_copy(p, h, kn, col, ht, &s_colbar[h]);
         }
         // ---- FWHT over the 12 bucket bits, ascending (fwht_serial's stage order)
         fwht16(v);  // bits 0-3
@@ -479,8 +501,11 @@ int fwht1p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, bool
   p.bmask = bmask;
   p.part = part;
   p.vec16 = 0;  // per operand: 16-byte copies of contiguous columns
+  p.bulk = 0;
   if (p.is[0] == 1 && p.ks[0] % 2 == 0 && n1 % 2 == 0 && (uintptr_t)p.X[0] % 16 == 0) p.vec16 |= 1;
   if (p.is[1] == 1 && p.ks[1] % 2 == 0 && n2 % 2 == 0 && (uintptr_t)p.X[1] % 16 == 0) p.vec16 |= 2;
+  static const bool no_bulk = getenv("SMM_NO_BULK_COLUMNS") != nullptr;
+  if (!no_bulk) p.bulk = p.vec16;  // contiguous, 16-byte aligned rows of a multiple of 16 bytes
   const size_t smem = (size_t)(2 * XS + ((n1 + 2) & ~1) + n2 + 1) * 8;
   SMM_CUDA_TRY(cudaFuncSetAttribute(fwht1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "fwht1p smem");

@@ -93,6 +93,50 @@ static __device__ __forceinline__ void ld2_hint(const double *p, double &a, doub
                : "memory");
 }
 
+// ---- TMA bulk copy global -> shared, completion counted on an mbarrier (one elected thread
+// issues; every consumer waits on the barrier's phase parity)
+static __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+static __device__ __forceinline__ void bulk_copy_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  // earlier generic-proxy accesses of dst (ordered before this thread by a barrier) come first
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+// two bulk copies counted on one barrier phase (one arrival with the total byte count)
+static __device__ __forceinline__ void bulk_copy2_g2s(void *dst0, const void *src0, uint32_t bytes0, void *dst1,
+                                                      const void *src1, uint32_t bytes1, uint64_t *bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes0 + bytes1) : "memory");
+  if (bytes0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst0)),
+                 "l"(src0), "r"(bytes0), "r"(b)
+                 : "memory");
+  if (bytes1)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst1)),
+                 "l"(src1), "r"(bytes1), "r"(b)
+                 : "memory");
+}
+static __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+}
+
 // Sum over the 32 lanes of a warp, for each of 32 registers: recursive halving
 // through shuffles (31 double shuffles per lane, no shared memory).  Step
 // (L, R): lanes differing in lane bit L exchange register halves [0, R) / [R, 2R).
