@@ -223,11 +223,15 @@ def run_reference(args) -> None:
     w = _cpu_instance(args.config)
     times = []
     info = None
-    for step in range(args.warmup + args.steps):
+    # warm-up steps: a bounded sample of the same work (the C port has no JIT; this warms the
+    # OpenMP pool and the caches), so the driver's W warm-ups do not cost W full products
+    for step in range(args.warmup):
+        ms, _ = _oracle_sample(w, min(w.n, 512), min(w.n, 512), threads)
+        print(f"reference warm-up {step}: sample (k 512, rows 512)", file=sys.stderr, flush=True)
+    for step in range(args.steps):
         ms, info = _oracle_full(w, threads)
         print(f"reference step {step}: {ms:.0f} ms {info}", file=sys.stderr, flush=True)
-        if step >= args.warmup:
-            times.append(ms)
+        times.append(ms)
     value = float(np.median(times))
     sample = (f"oracle C/OpenMP port (bit-exact vs reference Numba kernels) on {threads} host threads: the full "
               f"n={w.n} product every step (A^T copy, compress over all inner indices, inverse, all n^2 "
