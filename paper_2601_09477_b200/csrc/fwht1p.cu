@@ -148,7 +148,9 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
   const bool bulk = (p.bulk >> h) & 1 && p.n[h] > 0;
   uint32_t colpar = 0;  // phase parity of the next bulk copy
   const uint32_t col_s = (uint32_t)__cvta_generic_to_shared(col);
-  double *cells = X + 17 * ht;  // this thread's 16 buckets [16 ht, 16 ht + 16) in the padded layout
+  // this thread's 16 bucket cells (buckets 16 ht + j at X[j * 256 + ht]: the bank depends on the
+  // thread only, so the scatter's cell stores are conflict-free whatever buckets the lanes hit)
+  double *cells = X + ht;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_tmem)));
@@ -209,15 +211,15 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             run = ((w[r] & W_FIRST) ? 0.0 : run) + x[r];  // the reference's buckets start at 0.0
-            if (w[r] & W_LAST) cells[(w[r] >> 17) & 15u] = run;
+            if (w[r] & W_LAST) cells[((w[r] >> 17) & 15u) << 8] = run;
           }
         }
         double v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? cells[j] : 0.0;
+        for (int j = 0; j < 16; ++j) v[j] = ((mask >> j) & 1u) ? cells[j << 8] : 0.0;
+        bar_half(h);  // every cell is read before the exchange reuses the area
         if (t == d - 1) {
-          // every gather of column k done by the half: copy column k + 1 while k finishes
-          bar_half(h);
+          // every gather of column k done by the half (barrier above): copy column k + 1 while k finishes
           int64_t kn = k + 1;
           if (kn >= k_hi) {
             const int64_t tn = tile + gridDim.x;
