@@ -198,8 +198,10 @@ def test_guard_regions_untouched_and_runs_bit_reproducible():
     a = torch.as_tensor(rng.standard_normal((n, n)), device="cuda")
     bt = torch.as_tensor(rng.standard_normal((n, n)), device="cuda")
     G = 1 << 16
-    for tr, log2b, d in (("fwht", 12, 3), ("fwht", 16, 5), ("fwht", 17, 3), ("fft", 12, 3), ("fft", 15, 3),
-                         ("fwht", 6, 3), ("fft", 6, 3), ("fwht", 9, 65)):
+    # kernel families: fwht1p / fft1p (b = 2^12, one launch and repetition groups), fwht2p plain
+    # and folded, fft2p plain and folded, the v1 fold kernels (b < 2^8), d > 63
+    for tr, log2b, d in (("fwht", 12, 3), ("fwht", 12, 9), ("fwht", 16, 5), ("fwht", 17, 3), ("fft", 12, 3),
+                         ("fft", 12, 9), ("fft", 15, 3), ("fwht", 6, 3), ("fft", 6, 3), ("fwht", 9, 65)):
         b = 1 << log2b
         v = _lib.VARIANT[tr]
         words = O.draw_words(9, d, b)
