@@ -69,44 +69,58 @@ __global__ void csr_count_kernel(SketchHashes h, int64_t n1, int64_t n2, int32_t
   }
 }
 
-// exclusive scan of one (t, op) row of bucket counts per 1024-thread block: each
-// thread owns a contiguous chunk (sum, one block-wide scan of the chunk sums,
-// then the chunk's offsets) — two barriers instead of two per element batch
+// exclusive scan of one (t, op) row of bucket counts per 1024-thread block: chunks of 4096
+// counts, each thread loading 4 consecutive ones as one int4 (coalesced across the block),
+// a warp-shuffle scan and one block-wide combine per chunk, the running total carried
+// across chunks (b >= 4096 is a multiple of 4096; smaller rows take the scalar tail)
 __global__ void csr_scan_kernel(const int32_t *cnt, int32_t *off, int64_t b) {
   __shared__ int32_t wsum[32];
+  __shared__ int32_t s_carry;
   const int64_t row = blockIdx.x;  // (t, op)
   const int32_t *c = cnt + row * b;
   int32_t *o = off + row * (b + 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t per = (b + 1023) / 1024;
-  const int64_t lo = threadIdx.x * per < b ? threadIdx.x * per : b;
-  const int64_t hi = lo + per < b ? lo + per : b;
-  int32_t sum = 0;
-  for (int64_t i = lo; i < hi; ++i) sum += c[i];
-  int32_t inc = sum;  // inclusive scan within the warp
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc += y;
-  }
-  if (lane == 31) wsum[warp] = inc;
+  if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
-  if (warp == 0) {
-    int32_t w = wsum[lane];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, w, d);
-      if (lane >= d) w += y;
+  for (int64_t c0 = 0; c0 < b; c0 += 4096) {
+    const int64_t i0 = c0 + 4 * (int64_t)threadIdx.x;
+    int32_t v[4] = {0, 0, 0, 0};
+    if (i0 + 3 < b && (b & 3) == 0) {
+      const int4 q = *reinterpret_cast<const int4 *>(c + i0);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      for (int j = 0; j < 4; ++j) v[j] = i0 + j < b ? c[i0 + j] : 0;
     }
-    wsum[lane] = w;  // inclusive over warps
+    const int32_t sum = v[0] + v[1] + v[2] + v[3];
+    int32_t inc = sum;  // inclusive scan within the warp
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, inc, dd);
+      if (lane >= dd) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = wsum[lane];
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, dd);
+        if (lane >= dd) w += y;
+      }
+      wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int32_t carry = s_carry;
+    int32_t run = carry + inc - sum + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j < b) o[i0 + j] = run;
+      run += v[j];
+    }
+    __syncthreads();  // every thread has read wsum and s_carry
+    if (threadIdx.x == 0) s_carry = carry + wsum[31];
+    __syncthreads();
   }
-  __syncthreads();
-  int32_t run = inc - sum + (warp > 0 ? wsum[warp - 1] : 0);
-  for (int64_t i = lo; i < hi; ++i) {
-    o[i] = run;
-    run += c[i];
-  }
-  if (threadIdx.x == 1023) o[b] = wsum[31];
+  if (threadIdx.x == 0) o[b] = s_carry;
 }
 
 __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const int32_t *off, int32_t *fill,
