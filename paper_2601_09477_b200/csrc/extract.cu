@@ -138,24 +138,38 @@ __global__ void __launch_bounds__(XT) extract_kernel(ExtractArgs p) {
 
 // exclusive scan of per-row counts (single block) -> offsets; total -> *count
 __global__ void row_scan_kernel(const int64_t *rowcnt, int64_t rows, int64_t *offs, int64_t *count) {
-  __shared__ int64_t s[1024];
+  // exclusive scan of the per-row heavy-hitter counts: chunks of 1024 rows, warp-shuffle scans
+  // and one block-wide combine per chunk, the running total carried across chunks
+  __shared__ int64_t wsum[32];
   __shared__ int64_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int64_t base = 0; base < rows; base += 1024) {
     const int64_t r = base + threadIdx.x;
-    int64_t v = r < rows ? rowcnt[r] : 0;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      int64_t add = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
-      __syncthreads();
-      s[threadIdx.x] += add;
-      __syncthreads();
+    const int64_t v = r < rows ? rowcnt[r] : 0;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    if (r < rows) offs[r] = carry + s[threadIdx.x] - v;
+    if (lane == 31) wsum[warp] = inc;
     __syncthreads();
-    if (threadIdx.x == 1023) carry += s[1023];
+    if (warp == 0) {
+      int64_t w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int64_t c = carry;
+    if (r < rows) offs[r] = c + inc - v + (warp > 0 ? wsum[warp - 1] : 0);
+    __syncthreads();  // every thread has read wsum and carry
+    if (threadIdx.x == 0) carry = c + wsum[31];
     __syncthreads();
   }
   if (threadIdx.x == 0) *count = carry;
@@ -167,6 +181,7 @@ __global__ void hh_write_kernel(const uint32_t *mask, int64_t mask_ld, const int
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool a16 = ((uintptr_t)pairs & 15) == 0;  // caller's buffer allows 16-byte stores
   for (int64_t r = warp; r < rows; r += nwarps) {
     int64_t pos = offs[r];
     const uint32_t *mrow = mask + r * mask_ld;
@@ -186,8 +201,12 @@ __global__ void hh_write_kernel(const uint32_t *mask, int64_t mask_ld, const int
         bb &= bb - 1;
         const int64_t jj = w * 32 + bit;
         if (p0 < cap && jj < n2) {
-          pairs[2 * p0] = r0 + r;
-          pairs[2 * p0 + 1] = jj;
+          if (a16) {  // one 16-byte store per (i, j) pair
+            *reinterpret_cast<longlong2 *>(pairs + 2 * p0) = make_longlong2(r0 + r, jj);
+          } else {
+            pairs[2 * p0] = r0 + r;
+            pairs[2 * p0 + 1] = jj;
+          }
         }
         ++p0;
       }
