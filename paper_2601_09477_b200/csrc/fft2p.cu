@@ -135,6 +135,16 @@ __device__ __forceinline__ Head head(const Args &p, int t, int item) {
 // j = tile position & 15) — a register target would need a jump per entry.  Entries
 // are sorted by position: the first of a position stores, later ones add.  Returns the
 // mask of positions written.
+// fold character w_b^e of a gathered entry (e = a m mod b < 2^20): three shared tables,
+// w_b^e = s_tf2[e >> 14] * s_tf1[(e >> 7) & 127] * s_tf0[e & 127], filled once per CTA
+__shared__ double2 s_tf0[128], s_tf1[128], s_tf2[64];
+
+__device__ __forceinline__ double2 fold_twiddle(uint32_t e) {
+  const double2 a = s_tf2[e >> 14], b = s_tf1[(e >> 7) & 127u], c = s_tf0[e & 127u];
+  const double2 ab = make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+  return make_double2(fma(ab.x, c.x, -ab.y * c.y), fma(ab.x, c.y, ab.y * c.x));
+}
+
 template <int OP, bool FOLD>
 __device__ __forceinline__ void pull(const Args &p, int kappa, int t, const Head &hd, int a, double *S,
                                      uint32_t &mask) {
@@ -171,7 +181,7 @@ __device__ __forceinline__ void pull(const Args &p, int kappa, int t, const Head
         const bool have = (mask >> j) & 1u;
         if (FOLD) {
           const uint32_t m = eval_bucket(p.h.f[OP][t], (uint64_t)(es[s] & 0x03ffffffu), p.B);
-          const double2 w = __ldg((const double2 *)p.twb + (((uint32_t)a * m) & bmask));
+          const double2 w = fold_twiddle(((uint32_t)a * m) & bmask);
           const double cr = OP ? -val * w.y : val * w.x;
           const double ci = OP ? val * w.x : val * w.y;
           col[j * 64] = (have ? col[j * 64] : 0.0) + cr;
@@ -512,6 +522,18 @@ __global__ void __launch_bounds__(THREADS, 2) fft2p_kernel(Args p) {
   __shared__ int s_item[8];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  if (FOLD) {  // w_b^e for e = l, 128 l (l < 128) and 16384 l (l < 64)
+    for (int x = tid; x < 320; x += THREADS) {
+      const int l = x < 128 ? x : (x < 256 ? x - 128 : x - 256);
+      const double e = x < 128 ? (double)l : (x < 256 ? 128.0 * l : 16384.0 * l);
+      double sn, cs;
+      sincospi(-2.0 * e / (double)p.bfull, &sn, &cs);
+      const double2 w = make_double2(cs, sn);
+      if (x < 128) s_tf0[l] = w;
+      else if (x < 256) s_tf1[l] = w;
+      else s_tf2[l] = w;
+    }
+  }
   if (!FOLD) {  // w_b^l and w_b^(128 h), l, h < 128 (exact dyadic arguments, as twiddle_b_kernel)
     const double e = tid < 128 ? (double)tid : (double)(128 * (tid - 128));
     double sn, cs;
