@@ -615,6 +615,7 @@ __device__ __forceinline__ void gather_first2(const TwoPassArgs &p, int kappa, i
   }
 }
 
+template <bool FOLD>
 __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int op, int blk,
                                             double2 *S, const PullHead &hd, double2 (&xpre)[PGB], bool have_pre,
                                             const PullHead *next) {
@@ -657,7 +658,7 @@ __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int
       if (eb + s < cnt) {
         const int j = (int)((es[s] >> 26) & 15u);
         uint32_t neg = es[s] >> 31;
-        if (p.F > 1)  // fold character of slice a: (-1)^popcount(a & (h(i) >> LB))
+        if (FOLD)  // fold character of slice a: (-1)^popcount(a & (h(i) >> LB))
           neg ^= __popc((eval_bucket(p.h.f[op][t], (uint64_t)(es[s] & 0x03ffffffu), p.B) >> p.LB) & (uint32_t)a) & 1u;
         const double2 val = neg ? make_double2(-x[s].x, -x[s].y) : x[s];
         const double2 old = j == prevj ? col[j * 16] : make_double2(0.0, 0.0);  // 0 + val == val
@@ -697,12 +698,13 @@ __device__ __forceinline__ void p1_operand2(const TwoPassArgs &p, int kappa, int
   PROF_MARK(7);
 }
 
+template <bool FOLD>
 __device__ __forceinline__ void p1_item2(const TwoPassArgs &p, int kappa, int t, int a, int slot, int blk, double2 *S,
                                          const PullHead &hd1, const PullHead &hd0) {
   double2 xpre[PGB];
-  p1_operand2(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
+  p1_operand2<FOLD>(p, kappa, t, a, slot, 0, blk, S, hd0, xpre, false, &hd1);
   __syncthreads();  // every warp has read operand 0's exchange data from S
-  p1_operand2(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
+  p1_operand2<FOLD>(p, kappa, t, a, slot, 1, blk, S, hd1, xpre, true, nullptr);
 }
 
 // Pass 2 of slice s, pair mapping: slice position pi (8 bits) is bucket
@@ -821,7 +823,8 @@ __device__ __forceinline__ void red_add(int *ptr, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
 }
 
-template <int HB, bool PAIR>
+// FOLD (pair mapping only): b > 2^16, every entry carries its slice's fold character
+template <int HB, bool PAIR, bool FOLD = false>
 __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   extern __shared__ __align__(16) double S[];  // 8 warps x 32 x 32 doubles = 64 KB
   __shared__ uint32_t s_tmem;
@@ -971,7 +974,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     }
     const int *acc_flag = acc_cnt + (t * p.F + asl) * p.nblk + idx;
     if constexpr (PAIR) {
-      if (is_p1) p1_item2(p, kappa, t, asl, slot, idx, (double2 *)S, hd_cur1, hd_cur);
+      if (is_p1) p1_item2<FOLD>(p, kappa, t, asl, slot, idx, (double2 *)S, hd_cur1, hd_cur);
       else p2_item2<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, acc_ok, (double2 *)S);
     } else {
       if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
@@ -1194,8 +1197,19 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
                  "fwht2p smem");                                                                                \
     fwht2p_kernel<H, true><<<G, P_THREADS, smem, s>>>(p);                                                       \
     break;
-    SMM_LAUNCH_PAIR(0) SMM_LAUNCH_PAIR(1) SMM_LAUNCH_PAIR(2) SMM_LAUNCH_PAIR(3) SMM_LAUNCH_PAIR(4) SMM_LAUNCH_PAIR(5) SMM_LAUNCH_PAIR(6) SMM_LAUNCH_PAIR(7) SMM_LAUNCH_PAIR(8)
+    SMM_LAUNCH_PAIR(0) SMM_LAUNCH_PAIR(1) SMM_LAUNCH_PAIR(2) SMM_LAUNCH_PAIR(3) SMM_LAUNCH_PAIR(4) SMM_LAUNCH_PAIR(5) SMM_LAUNCH_PAIR(6) SMM_LAUNCH_PAIR(7)
 #undef SMM_LAUNCH_PAIR
+    case 8:  // 2^16-bucket slices: b = 2^16, or b > 2^16 folded (the fold character is compiled in only there)
+      if (p.F > 1) {
+        SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<8, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem), "fwht2p smem");
+        fwht2p_kernel<8, true, true><<<G, P_THREADS, smem, s>>>(p);
+      } else {
+        SMM_CUDA_TRY(cudaFuncSetAttribute(fwht2p_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem), "fwht2p smem");
+        fwht2p_kernel<8, true><<<G, P_THREADS, smem, s>>>(p);
+      }
+      break;
     default: break;
   } else switch (p.hb) {
 #define SMM_LAUNCH_HB(H)                                                                                 \
