@@ -40,11 +40,14 @@ constexpr int P1_BITS = 8;
 // P2(u) is dispensed `lag` groups after P1(u) (ring_plan(): 1 at b = 2^16, where 2 was
 // measured slower; small transforms have few items per unit and need more units in flight)
 
-// Optional phase profiler (env SMM_PROFILE=1): thread 0 of every CTA accumulates
-// clock64 deltas between marks; printed by the host after the launch.
+// Optional phase profiler: thread 0 of every CTA accumulates clock64 deltas between
+// marks, printed by the host after the launch.  Compiled in only with -DSMM_FWHT2P_PROFILE
+// (tools/prof_phases.sh builds that variant) and then switched on by SMM_PROFILE=1: the
+// runtime test of the marks alone cost the product kernel 2.7 % on cfg3 (40.66 vs 39.55 ms).
 __shared__ long long s_prof[16];
 __shared__ long long s_prof_last;
 __device__ int g_prof_on;
+#ifdef SMM_FWHT2P_PROFILE
 #define PROF_MARK(k)                                 \
   do {                                               \
     if (g_prof_on && threadIdx.x == 0) {             \
@@ -53,6 +56,11 @@ __device__ int g_prof_on;
       s_prof_last = _n;                              \
     }                                                \
   } while (0)
+#else
+#define PROF_MARK(k) \
+  do {               \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ CSR plan
 // entries sorted by (bucket, i) per (t, op): off [d][2][b+1], ent [d][2][nmax] = i | sign << 31
@@ -897,9 +905,13 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   // accumulator counter is only recorded — if incomplete the P2 item waits for it at its end
   auto deps_settle = [&](Deps &D) {
     if (D.ptr[0] && D.val[0] < D.tgt[0]) {
+#ifdef SMM_FWHT2P_PROFILE
       const long long w0 = g_prof_on ? clock64() : 0;
+#endif
       while (ld_acquire(D.ptr[0]) < D.tgt[0]) __nanosleep(32);
+#ifdef SMM_FWHT2P_PROFILE
       if (g_prof_on) s_prof[11] += clock64() - w0;  // informational
+#endif
     }
     sh_ver[0] = D.ver[0];
     sh_ver[1] = D.ver[1];
@@ -1174,7 +1186,16 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     const int rc = l2_policies(p.pol_last, p.pol_first);
     if (rc) return rc;
   }
+#ifdef SMM_FWHT2P_PROFILE
   static const bool prof_on = getenv("SMM_PROFILE") != nullptr;
+#else
+  static const bool prof_on = false;
+  if (getenv("SMM_PROFILE")) {
+    static bool said = false;
+    if (!said) fprintf(stderr, "[fwht2p] SMM_PROFILE: this build has no phase marks (tools/prof_phases.sh)\n");
+    said = true;
+  }
+#endif
   if (prof_on) {
     cudaMalloc((void **)&p.prof, 16 * sizeof(long long));
     cudaMemset(p.prof, 0, 16 * sizeof(long long));

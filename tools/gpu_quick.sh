@@ -10,4 +10,4 @@ import json
 d = json.loads(open("gpurun_out/b.json").read().strip().splitlines()[-1])
 print("bench", d["ms_per_step"], d["breakdown_ms"], "frac", round(d["roofline"]["frac"], 4), d["clocks"])
 PY
-SMM_PROFILE=1 timeout -s KILL 300 python tools/prof_compress.py ${1:-cfg3} 2 2>&1 | tail -2
+bash tools/prof_phases.sh ${1:-cfg3}
