@@ -745,10 +745,18 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     }
     PROF_MARK(8);
     reg_fwht16x2(v, HB < 4 ? HB : 4);  // pi bits 0..min(hb, 4)-1
-    // last use of these Y rows (all read by this warp): drop the L2 lines without write-back
-    __syncwarp();
-    {
-      const double *rowp = Ys - 2 * kp + row_of(lane | (warp << 5)) * KT;
+    // Last use of these Y rows (all read by this warp): drop the L2 lines without write-back.
+    // Where the discard is issued matters: ptxas is free to move it right behind the loads
+    // (the PTX carries no dependency on their data), and a discard that reaches L2 while the
+    // rows are still being read measured 18 % slower on cfg3 (46.8 vs 39.5 ms); at the end of
+    // the item it is 2.3 % slower (the dirty lines live longer and are written back).  Full
+    // slices (hb = 8) issue it behind the exchange barrier, which no load of the rows can
+    // cross (cfg3 -0.5 %, cfg4 / b = 2^18..2^20 -1 %); narrower slices keep it before the
+    // barrier (b = 2^14: 2.9 % faster there).  profiles/r02_ab_discard_placement.txt
+    constexpr bool LATE_DISCARD = HB >= 8;
+    const double *rowp = Ys - 2 * kp + row_of(lane | (warp << 5)) * KT;
+    if constexpr (!LATE_DISCARD) {
+      __syncwarp();
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
     }
@@ -757,6 +765,10 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = S[((warp | (lb << 3) | (j << 4)) * 16) + kp];
+    if constexpr (LATE_DISCARD) {
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
+    }
     reg_fwht16x2(v, HB - 4);  // pi bits 4..hb-1
     if (op == 0) {
 #pragma unroll
