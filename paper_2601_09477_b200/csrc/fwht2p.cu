@@ -751,9 +751,11 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     // rows are still being read measured 18 % slower on cfg3 (46.8 vs 39.5 ms); at the end of
     // the item it is 2.3 % slower (the dirty lines live longer and are written back).  Full
     // slices (hb = 8) issue it behind the exchange barrier, which no load of the rows can
-    // cross (cfg3 -0.5 %, cfg4 / b = 2^18..2^20 -1 %); narrower slices keep it before the
-    // barrier (b = 2^14: 2.9 % faster there).  profiles/r02_ab_discard_placement.txt
-    constexpr bool LATE_DISCARD = HB >= 8;
+    // cross (cfg3 -0.5 %, cfg4 / b = 2^18..2^20 -1 %), and so do the narrowest ones (hb <= 2:
+    // hardly any butterflies stand between their loads and the discard; b = 2^10 -4 %); the
+    // others keep it before the barrier (b = 2^14: 2.9 % faster there).
+    // profiles/r02_ab_discard_placement.txt
+    constexpr bool LATE_DISCARD = HB >= 8 || HB <= 2;
     const double *rowp = Ys - 2 * kp + row_of(lane | (warp << 5)) * KT;
     if constexpr (!LATE_DISCARD) {
       __syncwarp();
