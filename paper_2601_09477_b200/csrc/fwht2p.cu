@@ -149,6 +149,24 @@ __global__ void csr_fill_kernel(SketchHashes h, int64_t n1, int64_t n2, const in
   }
 }
 
+// CSR heads for the pair mapping: per (t, op) and 16-bucket group, its range and first 16 entry
+// words in one record, so that a pass-1 item's heads are independent loads that cp.async can
+// stage in shared memory (fwht2p_kernel: "CSR heads")
+__global__ void csr_heads_kernel(const int32_t *off, const uint32_t *ent, int64_t nmax, int64_t b, int rows,
+                                 uint32_t *hw, int2 *hr) {
+  const int64_t ng = b / 16;
+  const int64_t total = (int64_t)rows * ng * 16;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(x & 15);
+    const int64_t rg = x >> 4;
+    const int64_t row = rg / ng, g = rg % ng;
+    const int32_t *o = off + row * (b + 1) + g * 16;
+    const int e_lo = o[0], e_hi = o[16];
+    hw[x] = e_lo + j < e_hi ? ent[row * nmax + e_lo + j] : 0u;
+    if (j == 0) hr[rg] = make_int2(e_lo, e_hi);
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 // x / d for 0 <= x < 2^31 by multiply-high (the scheduler thread decodes an item
 // on the critical path of every CTA barrier; 32-bit division costs ~20 instructions)
@@ -179,6 +197,8 @@ struct TwoPassArgs {
   FastDiv div_df, div_F, div_slot;
   const int32_t *off;
   const uint32_t *ent;
+  const uint32_t *hw;  // pair mapping: first 16 entry words of every 16-bucket group [d][2][bsz / 16][16]
+  const int2 *hr;      // and the group's CSR range (e_lo, e_hi) [d][2][bsz / 16]
   int64_t nmax, bsz;
   double *Y;   // [nslot][2][b][KT]
   double *acc; // [d][b]
@@ -851,6 +871,10 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   extern __shared__ __align__(16) double S[];  // 8 warps x 32 x 32 doubles = 64 KB
   __shared__ uint32_t s_tmem;
   __shared__ int s_item[12];
+  // CSR heads of the next pass-1 item (SMEM_HEADS below), staged by cp.async while the current
+  // item computes: no register holds them across the item and no warp waits for their loads
+  __shared__ __align__(16) uint32_t s_hw[2][2][256];
+  __shared__ __align__(16) int2 s_hr[2][2][16];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (warp == 0) {
@@ -945,8 +969,17 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  PullHead hd_next, hd_next1;  // both operands' CSR heads of the next pass-1 item
+  // Both operands' CSR heads of the next pass-1 item are fetched one item ahead.  In registers
+  // (hd_next*) the second-level load (entry words) waits for the first (bucket offsets) and
+  // ptxas spills the results at once — a store that waits for them: two L2 round trips at the
+  // start of every item (7 % of all warp samples on cfg3).  Full slices of the pair mapping
+  // therefore stage the plan's per-group head records (csr_heads_kernel) in shared memory with
+  // cp.async: no register, no wait (cfg3 39.2 -> 38.1 ms, cfg4 501 -> 490 ms; at b = 2^14 the
+  // register path measured 1.9 % faster and stays).  profiles/r02_ab_smem_heads.txt
+  constexpr bool SMEM_HEADS = PAIR && HB >= 8;
+  PullHead hd_next, hd_next1;
   bool hd_valid = false;
+  int hbuf = 0;  // the s_hw / s_hr buffer holding the next pass-1 item's heads
   while (true) {
     if (tid == 0) {
       const Item it = itn;
@@ -989,14 +1022,43 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     if (!go) break;
     PullHead hd_cur, hd_cur1;
     auto head = [&](int tt, int op, int blk) { return PAIR ? pull_head2(p, tt, op, blk) : pull_head(p, tt, op, blk); };
-    if (is_p1) {
-      hd_cur = hd_valid ? hd_next : head(t, 0, idx);
-      hd_cur1 = hd_valid ? hd_next1 : head(t, 1, idx);
-    }
-    hd_valid = next_p1 != 0;
-    if (hd_valid) {  // land while this item computes
-      hd_next = head(next_t, 0, next_idx);
-      hd_next1 = head(next_t, 1, next_idx);
+    if constexpr (SMEM_HEADS) {
+      if (is_p1) {
+        if (hd_valid) {
+          const int g = (tid >> 4);  // this half-warp's 16-bucket group within the block
+          const int2 r0 = s_hr[hbuf][0][g], r1 = s_hr[hbuf][1][g];
+          hd_cur.e_lo = r0.x; hd_cur.e_hi = r0.y; hd_cur.first = s_hw[hbuf][0][tid];
+          hd_cur1.e_lo = r1.x; hd_cur1.e_hi = r1.y; hd_cur1.first = s_hw[hbuf][1][tid];
+        } else {
+          hd_cur = head(t, 0, idx);
+          hd_cur1 = head(t, 1, idx);
+        }
+      }
+      hd_valid = next_p1 != 0;
+      if (hd_valid) {  // land while this item computes (waited for before [B])
+        hbuf ^= 1;
+        if (tid < 144) {
+          const int op = tid >= 72 ? 1 : 0;
+          const int r = tid - 72 * op;
+          const int64_t ng = p.bsz >> 4;
+          const int64_t rg = ((int64_t)next_t * 2 + op) * ng + (int64_t)next_idx * 16;
+          const void *src = r < 64 ? (const void *)(p.hw + rg * 16 + r * 4) : (const void *)(p.hr + rg + (r - 64) * 2);
+          const void *dst = r < 64 ? (const void *)(&s_hw[hbuf][op][r * 4]) : (const void *)(&s_hr[hbuf][op][(r - 64) * 2]);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    } else {
+      if (is_p1) {
+        hd_cur = hd_valid ? hd_next : head(t, 0, idx);
+        hd_cur1 = hd_valid ? hd_next1 : head(t, 1, idx);
+      }
+      hd_valid = next_p1 != 0;
+      if (hd_valid) {  // land while this item computes
+        hd_next = head(next_t, 0, next_idx);
+        hd_next1 = head(next_t, 1, next_idx);
+      }
     }
     const int *acc_flag = acc_cnt + (t * p.F + asl) * p.nblk + idx;
     if constexpr (PAIR) {
@@ -1015,6 +1077,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       for (int j = 0; j < 2; ++j)
         if (D.ptr[j]) D.val[j] = ld_relaxed(D.ptr[j]);
     }
+    if constexpr (SMEM_HEADS) asm volatile("cp.async.wait_group 0;" ::: "memory");  // the staged heads landed
     tc_fence_before();
     PROF_MARK(2);
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
@@ -1100,6 +1163,8 @@ int64_t fwht2p_workspace(int d, int log2b, int64_t n1, int64_t n2, int64_t K) {
   ring_plan(LB, U, lag, nslot);
   w += pad256((int64_t)nslot * 2 * bs * KT * 8);  // Y ring
   w += pad256((1 + 2 * U + (int64_t)d * F * nblk) * 4);       // counters
+  w += pad256((int64_t)d * 2 * (bs / 16) * 16 * 4);            // CSR heads: first words
+  w += pad256((int64_t)d * 2 * (bs / 16) * 8);                 // CSR heads: ranges
   return w;
 }
 
@@ -1135,6 +1200,10 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   ring_plan(LB, U, lag, nslot);
   q += pad256((int64_t)nslot * 2 * bs * KT * 8);
   int *ctr = (int *)q;
+  q += pad256((1 + 2 * U + (int64_t)d * F * (bs >> P1_BITS)) * 4);
+  uint32_t *hw = (uint32_t *)q;
+  q += pad256((int64_t)d * 2 * (bs / 16) * 16 * 4);
+  int2 *hr = (int2 *)q;
   const int nblk = (int)(bs >> P1_BITS);
   if (K <= 0) {
     if (!acc_add) SMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)d * b * 8, s), "acc memset");
@@ -1162,6 +1231,13 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     const int rc = csr_sort(off, ent, nmax, bs, d * 2, s);  // deterministic: increasing i per bucket
     if (rc) return rc;
   }
+  if (LB - P1_BITS >= 8) {  // full slices: the head records the kernel stages in shared memory (SMEM_HEADS)
+    const int64_t tot = (int64_t)d * 2 * bs;
+    int64_t hblocks = ceil_div(tot, 256);
+    if (hblocks > 8192) hblocks = 8192;
+    csr_heads_kernel<<<(unsigned)hblocks, 256, 0, s>>>(off, ent, nmax, bs, d * 2, hw, hr);
+    SMM_LAUNCH_CHECK("csr_heads_kernel");
+  }
   SMM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (size_t)(1 + 2 * U + (int64_t)d * F * nblk) * 4, s), "counter memset");
   TwoPassArgs p;
   p.h = h;
@@ -1186,6 +1262,8 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
   p.div_slot = make_fastdiv((uint32_t)nslot);
   p.off = off;
   p.ent = ent;
+  p.hw = hw;
+  p.hr = hr;
   p.nmax = nmax;
   p.bsz = bs;
   p.Y = Y;
