@@ -779,8 +779,11 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
     const double *rowp = Ys - 2 * kp + row_of(lane | (warp << 5)) * KT;
     if constexpr (!LATE_DISCARD) {
       __syncwarp();
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
+      // predicated on the phase-A results, so that ptxas cannot hoist it to the loads (the bit
+      // pattern is a NaN payload no transform produces; a skipped discard would cost nothing)
+      if (__double2hiint(v[0].x) != 0x7ff8dead) asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp) : "memory");
+      if (__double2hiint(v[15].y) != 0x7ff8dead)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(rowp + 16) : "memory");
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) cell[j * 16] = v[j];
@@ -861,6 +864,14 @@ __device__ __forceinline__ Item decode_item(const TwoPassArgs &p, int64_t pos, i
   return it;
 }
 
+// threadIdx.x read afresh (ptxas keeps the kernel-entry copy in a register it spills; the reload
+// from local memory missed L1 behind the gather stream: 3 % of all warp samples on cfg3)
+__device__ __forceinline__ int tid_now() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
 __device__ __forceinline__ void red_add(int *ptr, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
 }
@@ -913,6 +924,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   __shared__ Item sh_itn;
   __shared__ int sh_ver[2];  // highest unit whose completion thread 0 acquired: done1 (P2), done2 (P1)
   __shared__ int s_acc_ok;   // the next P2 item's accumulator counter was acquired complete
+  __shared__ int sh_prev_next;  // the previous descriptor's next_p1 (thread 0)
   int64_t &nxt = sh_nxt;
   Item &itn = sh_itn;
   struct Deps {
@@ -920,6 +932,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     int tgt[2], val[2];
     int ver[2];
   };
+  __shared__ Deps sD;
   auto deps_of = [&](const Item &it, Deps &D) {
     D.ptr[0] = D.ptr[1] = nullptr;
     D.tgt[0] = D.tgt[1] = D.val[0] = D.val[1] = 0;
@@ -960,6 +973,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     nxt = atomicAdd(ticket, 1);
     itn = decode_item(p, cur, log2g);
     sh_ver[0] = sh_ver[1] = -1;
+    sh_prev_next = 0;
     Deps D;  // the first item's dependencies (usually none)
     deps_of(itn, D);
     deps_settle(D);
@@ -970,13 +984,13 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   tc_fence_after();
   const uint32_t tmem = s_tmem;
   // Both operands' CSR heads of the next pass-1 item are fetched one item ahead.  In registers
-  // (hd_next*) the second-level load (entry words) waits for the first (bucket offsets) and
-  // ptxas spills the results at once — a store that waits for them: two L2 round trips at the
-  // start of every item (7 % of all warp samples on cfg3).  Full slices of the pair mapping
-  // therefore stage the plan's per-group head records (csr_heads_kernel) in shared memory with
-  // cp.async: no register, no wait (cfg3 39.2 -> 38.1 ms, cfg4 501 -> 490 ms; at b = 2^14 the
-  // register path measured 1.9 % faster and stays).  profiles/r02_ab_smem_heads.txt
-  constexpr bool SMEM_HEADS = PAIR && HB >= 8;
+  // (hd_next*, the one-k-per-lane mapping) the second-level load (entry words) waits for the
+  // first (bucket offsets) and ptxas spills the results at once — a store that waits for them:
+  // two L2 round trips at the start of every item (7 % of all warp samples on cfg3).  The pair
+  // mapping therefore stages the plan's per-group head records (csr_heads_kernel) in shared
+  // memory with cp.async: no register, no wait (cfg3 39.2 -> 38.1 ms, cfg4 501 -> 490 ms,
+  // cfg5 b = 2^14 -3.4 %).  profiles/r02_ab_smem_heads.txt
+  constexpr bool SMEM_HEADS = PAIR;
   PullHead hd_next, hd_next1;
   bool hd_valid = false;
   int hbuf = 0;  // the s_hw / s_hr buffer holding the next pass-1 item's heads
@@ -998,6 +1012,8 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       s_item[7] = (in.pos < total && in.is_p1) ? 1 : 0;
       s_item[8] = fdiv(un, p.div_F);
       s_item[9] = in.idx;
+      s_item[11] = sh_prev_next;  // this item's CSR heads were fetched during the previous item
+      sh_prev_next = s_item[7];
       itn = in;
     }
     tc_fence_before();
@@ -1017,6 +1033,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     const int is_p1 = s_item[1], u = s_item[2], idx = s_item[3];
     const int kappa = s_item[4], t = s_item[5], slot = s_item[6], asl = s_item[10];
     const int next_p1 = s_item[7], next_t = s_item[8], next_idx = s_item[9];
+    const bool hd_have = s_item[11] != 0;
     const int acc_ok = s_acc_ok && !p.acc_slow;
     if (tid == 0 && go) nxt = itn.pos < total ? (int64_t)atomicAdd(ticket, 1) : itn.pos;
     if (!go) break;
@@ -1024,7 +1041,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     auto head = [&](int tt, int op, int blk) { return PAIR ? pull_head2(p, tt, op, blk) : pull_head(p, tt, op, blk); };
     if constexpr (SMEM_HEADS) {
       if (is_p1) {
-        if (hd_valid) {
+        if (hd_have) {
           const int g = (tid >> 4);  // this half-warp's 16-bucket group within the block
           const int2 r0 = s_hr[hbuf][0][g], r1 = s_hr[hbuf][1][g];
           hd_cur.e_lo = r0.x; hd_cur.e_hi = r0.y; hd_cur.first = s_hw[hbuf][0][tid];
@@ -1034,8 +1051,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
           hd_cur1 = head(t, 1, idx);
         }
       }
-      hd_valid = next_p1 != 0;
-      if (hd_valid) {  // land while this item computes (waited for before [B])
+      if (next_p1) {  // land while this item computes (waited for before [B])
         hbuf ^= 1;
         if (tid < 144) {
           const int op = tid >= 72 ? 1 : 0;
@@ -1068,14 +1084,17 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       if (is_p1) p1_item(p, kappa, t, asl, slot, idx, S, hd_cur1, hd_cur);
       else p2_item<HB>(p, kappa, t, asl, slot, idx, tmem, acc_flag, acc_ok, S);
     }
-    // thread 0: relaxed probe of the next item's dependency counters (acquired by the fence below)
-    Deps D;
-    if (tid == 0) {
+    // thread 0: relaxed probe of the next item's dependency counters (acquired by the fence below);
+    // the probe state crosses [B] in shared memory, not in (spilled) registers
+    const int tid_t = tid_now();
+    if (tid_t == 0) {
+      Deps D;
       const Item nx = itn;
       deps_of(nx, D);
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         if (D.ptr[j]) D.val[j] = ld_relaxed(D.ptr[j]);
+      sD = D;
     }
     if constexpr (SMEM_HEADS) asm volatile("cp.async.wait_group 0;" ::: "memory");  // the staged heads landed
     tc_fence_before();
@@ -1083,7 +1102,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     __syncthreads();  // [B]: the block's writes are done; smem / TMEM may be reused
     PROF_MARK(10);
     tc_fence_after();
-    if (tid == 32) {
+    if (tid_t == 32) {
       // release this item's writes (covered through [B]), then publish it
       asm volatile("fence.release.gpu;" ::: "memory");
       if (is_p1) red_add(done1 + u, 1);
@@ -1092,10 +1111,11 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
         red_add(done2 + u, 1);
       }
     }
-    if (tid == 0) {
+    if (tid_t == 0) {
       // acquire the probed counters (PTX acquire pattern: relaxed reads, then an acquire fence;
       // no wait for outstanding stores), poll one that is not yet complete
       asm volatile("fence.acquire.gpu;" ::: "memory");
+      Deps D = sD;
       deps_settle(D);
     }
   }
@@ -1231,7 +1251,7 @@ int fwht2p_accumulate(const SketchHashes &h, const double *xa, int64_t lda, cons
     const int rc = csr_sort(off, ent, nmax, bs, d * 2, s);  // deterministic: increasing i per bucket
     if (rc) return rc;
   }
-  if (LB - P1_BITS >= 8) {  // full slices: the head records the kernel stages in shared memory (SMEM_HEADS)
+  {  // pair mapping: the head records the kernel stages in shared memory (SMEM_HEADS)
     const int64_t tot = (int64_t)d * 2 * bs;
     int64_t hblocks = ceil_div(tot, 256);
     if (hblocks > 8192) hblocks = 8192;
