@@ -1087,14 +1087,14 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     // thread 0: relaxed probe of the next item's dependency counters (acquired by the fence below);
     // the probe state crosses [B] in shared memory, not in (spilled) registers
     const int tid_t = tid_now();
+    int pv0 = 0, pv1 = 0;  // the probed values stay in registers (a store of them would wait for the loads before [B])
     if (tid_t == 0) {
       Deps D;
       const Item nx = itn;
       deps_of(nx, D);
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if (D.ptr[j]) D.val[j] = ld_relaxed(D.ptr[j]);
       sD = D;
+      if (D.ptr[0]) pv0 = ld_relaxed(D.ptr[0]);
+      if (D.ptr[1]) pv1 = ld_relaxed(D.ptr[1]);
     }
     if constexpr (SMEM_HEADS) asm volatile("cp.async.wait_group 0;" ::: "memory");  // the staged heads landed
     tc_fence_before();
@@ -1116,6 +1116,8 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       // no wait for outstanding stores), poll one that is not yet complete
       asm volatile("fence.acquire.gpu;" ::: "memory");
       Deps D = sD;
+      D.val[0] = pv0;
+      D.val[1] = pv1;
       deps_settle(D);
     }
   }
