@@ -968,6 +968,29 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     sh_ver[1] = D.ver[1];
     s_acc_ok = (!D.ptr[1] || D.val[1] >= D.tgt[1]) ? 1 : 0;
   };
+  // item descriptor (thread 0): item `it` (= itn) and the prefetch hint of its successor, decoded
+  // from the ticket claimed one item earlier.  Written before [B] of the previous item: every warp
+  // read the previous descriptor at that item's start, at least one CTA barrier ago.
+  auto describe = [&]() {
+    const Item it = itn;
+    const Item in = decode_item(p, nxt, log2g);
+    const int ut = fmod_(it.u, p.div_df);
+    const int un = fmod_(in.u, p.div_df);
+    s_item[0] = it.pos < total ? 1 : 0;
+    s_item[1] = it.is_p1;
+    s_item[2] = it.u;
+    s_item[3] = it.idx;
+    s_item[4] = fdiv(it.u, p.div_df);
+    s_item[5] = fdiv(ut, p.div_F);
+    s_item[6] = fmod_(it.u, p.div_slot);
+    s_item[10] = fmod_(ut, p.div_F);
+    s_item[7] = (in.pos < total && in.is_p1) ? 1 : 0;
+    s_item[8] = fdiv(un, p.div_F);
+    s_item[9] = in.idx;
+    s_item[11] = sh_prev_next;  // this item's CSR heads were fetched during the previous item
+    sh_prev_next = s_item[7];
+    itn = in;
+  };
   if (tid == 0) {
     const int64_t cur = atomicAdd(ticket, 1);
     nxt = atomicAdd(ticket, 1);
@@ -978,6 +1001,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
     deps_of(itn, D);
     deps_settle(D);
     s_acc_ok = 0;
+    describe();
   }
   tc_fence_before();
   __syncthreads();
@@ -995,27 +1019,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
   bool hd_valid = false;
   int hbuf = 0;  // the s_hw / s_hr buffer holding the next pass-1 item's heads
   while (true) {
-    if (tid == 0) {
-      const Item it = itn;
-      PROF_MARK(13);
-      const Item in = decode_item(p, nxt, log2g);
-      const int ut = fmod_(it.u, p.div_df);
-      const int un = fmod_(in.u, p.div_df);
-      s_item[0] = it.pos < total ? 1 : 0;
-      s_item[1] = it.is_p1;
-      s_item[2] = it.u;
-      s_item[3] = it.idx;
-      s_item[4] = fdiv(it.u, p.div_df);
-      s_item[5] = fdiv(ut, p.div_F);
-      s_item[6] = fmod_(it.u, p.div_slot);
-      s_item[10] = fmod_(ut, p.div_F);
-      s_item[7] = (in.pos < total && in.is_p1) ? 1 : 0;
-      s_item[8] = fdiv(un, p.div_F);
-      s_item[9] = in.idx;
-      s_item[11] = sh_prev_next;  // this item's CSR heads were fetched during the previous item
-      sh_prev_next = s_item[7];
-      itn = in;
-    }
+    PROF_MARK(13);
     tc_fence_before();
     PROF_MARK(0);
     // [A]: the item descriptor (thread 0, after acquiring the item's dependencies) reaches the
@@ -1095,6 +1099,7 @@ __global__ void __launch_bounds__(P_THREADS, 2) fwht2p_kernel(TwoPassArgs p) {
       sD = D;
       if (D.ptr[0]) pv0 = ld_relaxed(D.ptr[0]);
       if (D.ptr[1]) pv1 = ld_relaxed(D.ptr[1]);
+      describe();  // the next item's descriptor, while the probes fly
     }
     if constexpr (SMEM_HEADS) asm volatile("cp.async.wait_group 0;" ::: "memory");  // the staged heads landed
     tc_fence_before();
