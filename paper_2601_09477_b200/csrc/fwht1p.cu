@@ -145,6 +145,11 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
     mbar_init(&s_colbar[h], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // byte offset of the zero double past the column (the padding words' target), pinned in a register:
+  // ptxas otherwise re-reads p.n[h] with an indexed constant load inside the scatter loop, whose
+  // latency the loop then waits for (10 % of the kernel's warp samples)
+  uint32_t padw;
+  asm volatile("mov.u32 %0, %1;" : "=r"(padw) : "r"((uint32_t)(p.n[h] * 8)));
   const bool bulk = (p.bulk >> h) & 1 && p.n[h] > 0;
   uint32_t colpar = 0;  // phase parity of the next bulk copy
   const uint32_t col_s = (uint32_t)__cvta_generic_to_shared(col);
@@ -190,15 +195,18 @@ __global__ void __launch_bounds__(CT, 1) fwht1p_kernel(Args p) {
         const uint32_t *e2 = p.ent2 + p.roff[t * 2 + h] + tb.base + lane;
         const uint32_t mask = __ldg(p.bmask + (t * 2 + h) * HT + ht);
         double run = 0.0;
-        uint32_t wn[8];
+        uint32_t wn[8], wn2[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) wn[r] = r < tb.maxcnt ? __ldg(e2 + r * 32) : (uint32_t)(p.n[h] * 8);
+        for (int r = 0; r < 8; ++r) wn[r] = r < tb.maxcnt ? __ldg(e2 + r * 32) : padw;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) wn2[r] = 8 + r < tb.maxcnt ? __ldg(e2 + (8 + r) * 32) : padw;
         for (int q0 = 0; q0 < tb.maxcnt; q0 += 8) {
           uint32_t w[8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {  // the next batch's words are in flight while this one is added
+          for (int r = 0; r < 8; ++r) {  // the next two batches' words are in flight while this one is added
             w[r] = wn[r];
-            wn[r] = q0 + 8 + r < tb.maxcnt ? __ldg(e2 + (q0 + 8 + r) * 32) : (uint32_t)(p.n[h] * 8);
+            wn[r] = wn2[r];
+            wn2[r] = q0 + 16 + r < tb.maxcnt ? __ldg(e2 + (q0 + 16 + r) * 32) : padw;
           }
           double x[8];
 #pragma unroll
