@@ -756,12 +756,22 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
   const uint64_t pol = p.pol_first;
   double2 *cell = S + (warp * 32 + lb * 16) * 16 + kp;  // phase-A cells of this lane (j * 16 apart)
   double2 v[16];
-#pragma unroll 1
-  for (int op = 0; op < 2; ++op) {
-    const double *Ys = p.Y + ((int64_t)slot * 2 + op) * p.bsz * KT + 2 * kp;
+  // Narrower slices (hb < 8) issue operand 1's row loads before the "exchange area free" barrier
+  // of operand 0, so that they fly while the CTA meets there (operand loop unrolled; cfg5
+  // b = 2^14 5.18 -> 4.95 ms).  At hb = 8 the same costs 24 bytes of spills and 2 % (36.2 vs
+  // 35.5 ms on cfg3): full slices load at the top of each operand's turn.
+  constexpr bool EARLY_Y1 = HB < 8;
+  const double *Yb = p.Y + ((int64_t)slot * 2) * p.bsz * KT + 2 * kp;
+  if constexpr (EARLY_Y1) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      tp::ld2_hint(Ys + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
+    for (int j = 0; j < 16; ++j) tp::ld2_hint(Yb + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
+  }
+#pragma unroll(EARLY_Y1 ? 2 : 1)
+  for (int op = 0; op < 2; ++op) {
+    const double *Ys = Yb + (int64_t)op * p.bsz * KT;
+    if constexpr (!EARLY_Y1) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tp::ld2_hint(Ys + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
     }
     PROF_MARK(8);
     reg_fwht16x2(v, HB < 4 ? HB : 4);  // pi bits 0..min(hb, 4)-1
@@ -799,6 +809,11 @@ __device__ __forceinline__ void p2_item2(const TwoPassArgs &p, int kappa, int t,
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_st8(tq + col_fa + 16 * c, (const double *)(v + 4 * c));
       tmem_wait_st();
+      if constexpr (EARLY_Y1) {  // operand 1's rows fly while the CTA meets at the barrier
+        const double *Y1 = Yb + p.bsz * KT;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tp::ld2_hint(Y1 + row_of(j | (lb << 4) | (warp << 5)) * KT, v[j].x, v[j].y, pol);
+      }
       __syncthreads();  // S is reused by operand 1's exchange (the next item's waits for [B])
     }
   }
